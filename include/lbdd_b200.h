@@ -100,6 +100,8 @@ typedef struct lbdd_solve_report {
   /* device-side breakdown (B200 engine only; zero in the reference) */
   int64_t scan_ns;      /* validation + arrival scan + sort */
   int64_t relax_rounds; /* synchronous relaxation rounds executed */
+  int64_t grid_barriers; /* device-wide barriers executed by the engine */
+  int64_t device_ns;     /* CUDA-event time of the whole solve on its stream */
 } lbdd_solve_report;
 
 /* Opaque handle: one instance resident in HBM on one device. */
@@ -109,6 +111,8 @@ typedef struct lbdd_b200_instance lbdd_b200_instance;
 const char* lbdd_b200_version(void);
 const char* lbdd_b200_last_error(void);
 int lbdd_b200_device_count(void);
+/* Kernels of this library launched so far in this process (all devices). */
+long long lbdd_b200_launch_count(void);
 
 /* Upload an instance (host arrays) to `device`. Replaces constructing a
  * lbdd::ProblemInstance (core.hpp:130) — validation as in
@@ -182,6 +186,16 @@ lbdd_status lbdd_b200_build_index_device(lbdd_b200_instance* inst,
                                          const int32_t* d_assignment,
                                          int64_t row0, int64_t rows,
                                          int64_t* d_out, void* stream);
+
+/* Shard-resident variant for the multi-GPU build: `inst` holds only this
+ * rank's rows (global demand ids demand_offset .. demand_offset+n-1);
+ * d_assignment covers those rows; packed demand ids are global, so the
+ * per-rank k*k partials combine with an elementwise int64 MIN
+ * (ncclAllReduce / ncclMin over NVLink). */
+lbdd_status lbdd_b200_build_index_shard(lbdd_b200_instance* inst,
+                                        const int32_t* d_assignment,
+                                        int64_t demand_offset, int64_t* d_out,
+                                        void* stream);
 
 /* build_arrival_queue (solver.hpp:74-96): per demand the cheapest center
  * (smallest id on ties) and the arrival order sorted by (cost, demand).

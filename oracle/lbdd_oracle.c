@@ -1015,7 +1015,8 @@ int lbdd_oracle_arrival_queue(const lbdd_instance_desc* desc, int32_t* best_cent
 }
 
 int lbdd_oracle_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrivals,
-                             int64_t* elapsed_ns, int64_t* arrivals_done) {
+                             int32_t workers, int64_t* elapsed_ns, int64_t* arrivals_done) {
+  (void)workers; /* the port is single-threaded */
   ENTRY_BEGIN
   const Inst I = inst_from(desc);
   require_valid(&I);

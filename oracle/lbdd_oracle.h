@@ -61,8 +61,8 @@ int lbdd_oracle_generate(uint64_t seed, int64_t n, double ratio, double theta,
 /* Solve only the first `max_arrivals` arrivals of asral (bounded CPU
  * baseline sample); returns elapsed ns of the sampled loop. */
 int lbdd_oracle_asral_sample(const lbdd_instance_desc* desc,
-                             int64_t max_arrivals, int64_t* elapsed_ns,
-                             int64_t* arrivals_done);
+                             int64_t max_arrivals, int32_t workers,
+                             int64_t* elapsed_ns, int64_t* arrivals_done);
 
 #ifdef __cplusplus
 }

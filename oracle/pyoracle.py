@@ -163,12 +163,13 @@ class CLib:
                                               order.ctypes.data_as(_abi.I32P)))
         return bc, bcost, order
 
-    def asral_sample(self, inst, max_arrivals):
+    def asral_sample(self, inst, max_arrivals, workers=1):
+        """Time the first `max_arrivals` arrivals of asral_solve's main loop."""
         h = DescHolder(inst)
         ns = C.c_int64()
         done = C.c_int64()
-        self._check(self._fn("asral_sample")(h.ref, C.c_int64(max_arrivals), C.byref(ns),
-                                             C.byref(done)))
+        self._check(self._fn("asral_sample")(h.ref, C.c_int64(max_arrivals), C.c_int32(workers),
+                                             C.byref(ns), C.byref(done)))
         return ns.value, done.value
 
     def oracle_solve(self, inst, strict, size_limit=2000):

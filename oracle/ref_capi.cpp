@@ -352,12 +352,17 @@ extern "C" {
 // solver.hpp:135-167 verbatim in structure, stopped after `max_arrivals`
 // arrivals (no finish_report). Uses only the reference's own types.
 int lbdd_ref_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrivals,
-                          int64_t* elapsed_ns, int64_t* arrivals_done) {
+                          int32_t workers, int64_t* elapsed_ns, int64_t* arrivals_done) {
   return guarded([&] {
     const auto inst = to_instance(desc);
     lbdd::require_valid_instance(inst);
     const auto start = std::chrono::steady_clock::now();
+    lbdd::SolverOptions opts;
+    opts.parallel = workers > 1;  // para-asral: the reference's worker pool
+    opts.parallel_config.workers = workers;
+    lbdd::detail::EngineScope scope(opts, opts.parallel);
     lbdd::SolverState st(inst);
+    st.engine = scope.engine;
     auto queue = lbdd::detail::build_arrival_queue(inst);
     int64_t done = 0;
     while (!queue.empty() && done < max_arrivals) {

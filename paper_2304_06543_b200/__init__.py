@@ -15,7 +15,12 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # solver entry points load the CUDA library on first use (and fail loudly
     # when it is missing) — importing the package itself stays cheap.
-    from . import solver
+    if name.startswith("__"):
+        raise AttributeError(name)
+    import importlib
+    solver = importlib.import_module(__name__ + ".solver")
+    if name == "solver":
+        return solver
     if hasattr(solver, name):
         return getattr(solver, name)
     raise AttributeError(name)

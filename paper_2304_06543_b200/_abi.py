@@ -74,6 +74,8 @@ class SolveReportC(C.Structure):
         ("total_ns", C.c_int64),
         ("scan_ns", C.c_int64),
         ("relax_rounds", C.c_int64),
+        ("grid_barriers", C.c_int64),
+        ("device_ns", C.c_int64),
     ]
 
 

@@ -1,0 +1,1318 @@
+// Host side of the C ABI (include/lbdd_b200.h): validation, device memory,
+// launches, and the report — the reference's solver entry points
+// (solver.hpp:133-301) re-expressed over the device engine. All arithmetic
+// on the report path is exact 64-bit with the reference's overflow checks
+// (core.hpp:25-39).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <memory>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "lbdd_b200.h"
+
+// Single translation unit: the kernels are included, not linked.
+#include "engine.cu"
+#include "scan.cu"
+
+using namespace lbdd_b200;
+
+namespace capi_detail {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};  // kernels of this library launched
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void raise(int code, const std::string& m) { throw Error(code, m); }
+
+#define CUDA_OK(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t e__ = (expr);                                                           \
+    if (e__ != cudaSuccess) {                                                           \
+      raise(LBDD_ERR_CUDA, std::string("lbdd_b200: ") + #expr + ": " + cudaGetErrorString(e__)); \
+    }                                                                                   \
+  } while (0)
+
+template <typename F>
+lbdd_status guarded(F&& f) {
+  try {
+    f();
+    return LBDD_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<lbdd_status>(e.code);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LBDD_ERR_RUNTIME;
+  }
+}
+
+int64_t checked_add(int64_t a, int64_t b) {
+  int64_t r;
+  if (__builtin_add_overflow(a, b, &r)) raise(LBDD_ERR_OVERFLOW, "lbdd: cost accumulator overflow");
+  return r;
+}
+int64_t checked_mul(int64_t a, int64_t b) {
+  int64_t r;
+  if (__builtin_mul_overflow(a, b, &r)) raise(LBDD_ERR_OVERFLOW, "lbdd: cost accumulator overflow");
+  return r;
+}
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  void ensure(size_t c) {
+    if (c <= count && p) return;
+    release();
+    CUDA_OK(cudaMalloc(&p, std::max<size_t>(c, 1) * sizeof(T)));
+    count = c;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+};
+
+constexpr int kEngineThreads = 512;
+constexpr int kPieceRows = 256;
+constexpr int kMaxEngineK = 7000;      // shared-memory bound of the engine CTA
+constexpr int64_t kMaxPenalty = int64_t(1) << 40;  // packing bound (common.cuh)
+
+}  // namespace capi_detail
+using namespace capi_detail;
+
+// ---------------------------------------------------------------------------
+// instance
+// ---------------------------------------------------------------------------
+
+struct lbdd_b200_instance {
+  int device = 0;
+  int64_t n = 0, k = 0, pitch = 0;
+  int32_t* d_cm = nullptr;
+  bool owns_cm = false;
+  std::vector<int64_t> cap, off, par;
+  std::vector<int32_t> fam;
+  int64_t* d_cap = nullptr;
+  int32_t* d_fam = nullptr;
+  int64_t* d_off = nullptr;
+  int64_t* d_par = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+
+  // scan results
+  bool scanned = false;
+  int64_t min_cost = 0, max_cost = 0;
+  DevBuf<int32_t> best_center;
+  DevBuf<int64_t> keys, keys_sorted, minmax;
+  DevBuf<unsigned char> cub_tmp;
+
+  // engine state
+  DevBuf<int32_t> home, order, rowslot, src_list, inv_cnt, inv_cols, single_out, rowver;
+  DevBuf<int32_t> P[2][2];
+  DevBuf<int64_t> D[2][2], B[2][3];
+  DevBuf<int64_t> load, dummies, M, colW, single_gain;
+  DevBuf<EngineCtl> ctl;
+  DevBuf<GridBar> bar;
+  DevBuf<PathEdge> path;
+  DevBuf<uint8_t> dumflag;
+  // index build scratch
+  DevBuf<int32_t> ib_cnt, ib_off, ib_cursor, ib_sorted, ib_pc, ib_poff, ib_bad;
+  DevBuf<unsigned long long> obj_acc;
+  DevBuf<int32_t> obj_missing;
+
+  ~lbdd_b200_instance() {
+    cudaSetDevice(device);
+    if (owns_cm && d_cm) cudaFree(d_cm);
+    for (void* p : {static_cast<void*>(d_cap), static_cast<void*>(d_fam), static_cast<void*>(d_off),
+                    static_cast<void*>(d_par)}) {
+      if (p) cudaFree(p);
+    }
+    best_center.release(); keys.release(); keys_sorted.release(); minmax.release();
+    cub_tmp.release(); home.release(); order.release(); rowslot.release(); src_list.release();
+    inv_cnt.release(); inv_cols.release();
+    for (int s = 0; s < 2; ++s) {
+      for (int i = 0; i < 2; ++i) { P[s][i].release(); D[s][i].release(); }
+      for (int i = 0; i < 3; ++i) B[s][i].release();
+    }
+    single_out.release(); rowver.release(); load.release(); dummies.release(); M.release();
+    colW.release();
+    single_gain.release(); ctl.release(); bar.release(); path.release(); dumflag.release();
+    ib_cnt.release(); ib_off.release(); ib_cursor.release(); ib_sorted.release();
+    ib_pc.release(); ib_poff.release(); ib_bad.release(); obj_acc.release();
+    obj_missing.release();
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  int64_t pen_len(int64_t s) const { return off[s + 1] - off[s]; }
+
+  // PenaltySpec::at / total (core.hpp:60-95), host side, checked.
+  int64_t pen_at(int64_t s, int64_t j) const {
+    const int64_t* p = par.data() + off[s];
+    switch (fam[s]) {
+      case LBDD_PENALTY_CONSTANT: return p[0];
+      case LBDD_PENALTY_LINEAR: return checked_add(p[0], checked_mul(p[1], j - 1));
+      default: return p[std::min(j, pen_len(s)) - 1];
+    }
+  }
+  int64_t pen_total(int64_t s, int64_t m) const {
+    if (m <= 0) return 0;
+    const int64_t* p = par.data() + off[s];
+    switch (fam[s]) {
+      case LBDD_PENALTY_CONSTANT: return checked_mul(p[0], m);
+      case LBDD_PENALTY_LINEAR: {
+        const int64_t tri = checked_mul(m, m - 1) / 2;
+        return checked_add(checked_mul(p[0], m), checked_mul(p[1], tri));
+      }
+      default: {
+        int64_t sum = 0;
+        for (int64_t j = 1; j <= m; ++j) sum = checked_add(sum, pen_at(s, j));
+        return sum;
+      }
+    }
+  }
+  int64_t total_capacity() const {
+    int64_t t = 0;
+    for (auto c : cap) t += c;
+    return t;
+  }
+};
+
+namespace capi_detail {
+
+void upload_centers(lbdd_b200_instance* I, const lbdd_instance_desc* d) {
+  const int64_t k = d->k;
+  I->cap.assign(d->capacity, d->capacity + k);
+  I->fam.assign(d->penalty_family, d->penalty_family + k);
+  I->off.assign(d->penalty_offset, d->penalty_offset + k + 1);
+  const int64_t np = k > 0 ? I->off[k] : 0;
+  I->par.assign(d->penalty_params, d->penalty_params + np);
+  CUDA_OK(cudaMalloc(&I->d_cap, sizeof(int64_t) * std::max<int64_t>(k, 1)));
+  CUDA_OK(cudaMalloc(&I->d_fam, sizeof(int32_t) * std::max<int64_t>(k, 1)));
+  CUDA_OK(cudaMalloc(&I->d_off, sizeof(int64_t) * (k + 1)));
+  CUDA_OK(cudaMalloc(&I->d_par, sizeof(int64_t) * std::max<int64_t>(np, 1)));
+  if (k > 0) {
+    CUDA_OK(cudaMemcpy(I->d_cap, I->cap.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(I->d_fam, I->fam.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice));
+  }
+  CUDA_OK(cudaMemcpy(I->d_off, I->off.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice));
+  if (np > 0) CUDA_OK(cudaMemcpy(I->d_par, I->par.data(), sizeof(int64_t) * np, cudaMemcpyHostToDevice));
+}
+
+lbdd_b200_instance* new_instance(int device, int64_t n, int64_t k) {
+  auto* I = new lbdd_b200_instance();
+  I->device = device;
+  I->n = n;
+  I->k = k;
+  I->pitch = ((k + 3) / 4) * 4;
+  CUDA_OK(cudaSetDevice(device));
+  CUDA_OK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaDeviceGetAttribute(&I->num_sms, cudaDevAttrMultiProcessorCount, device));
+  return I;
+}
+
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
+}
+
+// validate_instance (core.hpp:250-305), center part; the matrix part runs
+// on the device inside the arrival scan.
+void validate_centers(const lbdd_b200_instance* I) {
+  auto fail = [](const std::string& m) {
+    raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: invalid instance: " + m);
+  };
+  if (I->k < 1) fail("instance has no service centers (k < 1)");
+  if (I->n < 1) fail("instance has no demand units (n < 1)");
+  for (int64_t s = 0; s < I->k; ++s) {
+    const std::string tag = "center " + std::to_string(s) + ": ";
+    const int64_t np = I->pen_len(s);
+    const int64_t* p = I->par.data() + I->off[s];
+    if (I->cap[s] < 0) fail(tag + "negative capacity");
+    switch (I->fam[s]) {
+      case LBDD_PENALTY_CONSTANT:
+        if (np != 1) fail(tag + "constant penalty takes one parameter");
+        else if (p[0] <= 0) fail(tag + "penalty not positive");
+        break;
+      case LBDD_PENALTY_LINEAR:
+        if (np != 2) fail(tag + "linear penalty takes two parameters");
+        else if (p[0] <= 0 || p[1] < 0) fail(tag + "penalty not positive");
+        break;
+      case LBDD_PENALTY_TABLE:
+        if (np == 0) {
+          fail(tag + "empty penalty table");
+        } else {
+          if (p[0] <= 0) fail(tag + "penalty not positive");
+          for (int64_t i = 1; i < np; ++i)
+            if (p[i] < p[i - 1]) fail(tag + "penalty not monotone");
+        }
+        break;
+      default: fail(tag + "bad penalty family");
+    }
+  }
+}
+
+// Device-range guards (not reference behaviour: the reference is int64
+// throughout; the device packs (cost, source) into one int64).
+void check_device_range(const lbdd_b200_instance* I) {
+  if (I->k > kMaxEngineK)
+    raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: engine supports k <= " + std::to_string(kMaxEngineK));
+  if (I->n >= INT32_MAX) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: n exceeds int32 demand ids");
+  for (int64_t s = 0; s < I->k; ++s) {
+    const int64_t* p = I->par.data() + I->off[s];
+    int64_t qmax = 0;
+    switch (I->fam[s]) {
+      case LBDD_PENALTY_CONSTANT: qmax = p[0]; break;
+      case LBDD_PENALTY_LINEAR: {
+        int64_t m, r;
+        if (__builtin_mul_overflow(p[1], I->n, &m) || __builtin_add_overflow(p[0], m, &r)) r = INT64_MAX;
+        qmax = r;
+        break;
+      }
+      default: qmax = p[I->pen_len(s) - 1]; break;
+    }
+    if (qmax > kMaxPenalty)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: penalty exceeds the device range (2^40)");
+  }
+}
+
+// Arrival scan + sort (build_arrival_queue, solver.hpp:89-96), with the
+// matrix half of validate_instance. Returns device time in ns.
+int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
+  const int64_t n = I->n;
+  I->best_center.ensure(n);
+  I->keys.ensure(n);
+  I->keys_sorted.ensure(n);
+  I->minmax.ensure(2);
+  const int64_t init[2] = {INT64_MAX, INT64_MIN};
+  cudaEvent_t e0, e1;
+  CUDA_OK(cudaEventCreate(&e0));
+  CUDA_OK(cudaEventCreate(&e1));
+  CUDA_OK(cudaEventRecord(e0, I->stream));
+  CUDA_OK(cudaMemcpyAsync(I->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 7) / 8, I->num_sms * 8));
+  g_launches++;
+  row_argmin_kernel<<<std::max(blocks, 1), 256, 0, I->stream>>>(
+      I->d_cm, I->pitch, n, static_cast<int32_t>(I->k), I->best_center.p, I->keys.p, I->minmax.p);
+  CUDA_OK(cudaGetLastError());
+  int64_t mm[2];
+  CUDA_OK(cudaMemcpyAsync(mm, I->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, I->stream));
+  CUDA_OK(cudaStreamSynchronize(I->stream));
+  I->min_cost = mm[0];
+  I->max_cost = mm[1];
+  if (validate_matrix && I->min_cost <= 0)
+    raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: invalid instance: non-positive cost in cost matrix");
+  // sort by (cost, demand): key bits = 32 (demand) + bits(max cost)
+  int end_bit = 32;
+  while (end_bit < 63 && (int64_t(1) << (end_bit - 32)) <= I->max_cost) ++end_bit;
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, reinterpret_cast<uint64_t*>(I->keys.p),
+                                 reinterpret_cast<uint64_t*>(I->keys_sorted.p),
+                                 static_cast<int>(n), 0, end_bit, I->stream);
+  I->cub_tmp.ensure(tmp_bytes);
+  cub::DeviceRadixSort::SortKeys(I->cub_tmp.p, tmp_bytes, reinterpret_cast<uint64_t*>(I->keys.p),
+                                 reinterpret_cast<uint64_t*>(I->keys_sorted.p),
+                                 static_cast<int>(n), 0, end_bit, I->stream);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaEventRecord(e1, I->stream));
+  CUDA_OK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  I->scanned = true;
+  return static_cast<int64_t>(ms * 1e6);
+}
+
+void fill64(lbdd_b200_instance* I, int64_t* p, int64_t count, int64_t v) {
+  g_launches++;
+  fill_i64_kernel<<<grid_for(count), 256, 0, I->stream>>>(p, count, v);
+  CUDA_OK(cudaGetLastError());
+}
+
+// build_index over the rows [r0, r1) of a device allotment into d_M (k*k,
+// pre-filled with kEmpty by the caller). Phase 1 buckets the demands by
+// home (histogram, scan, scatter, pieces); phase 2 is the matrix scan.
+void build_index_prepare(lbdd_b200_instance* I, const int32_t* d_home, int64_t r0, int64_t r1,
+                         cudaStream_t st, bool check) {
+  const int32_t k = static_cast<int32_t>(I->k);
+  const int64_t n = I->n;
+  I->ib_cnt.ensure(k + 1);
+  I->ib_off.ensure(k + 1);
+  I->ib_cursor.ensure(k + 1);
+  I->ib_pc.ensure(k + 1);
+  I->ib_poff.ensure(k + 1);
+  I->ib_sorted.ensure(std::max<int64_t>(n, 1));
+  I->ib_bad.ensure(1);
+  CUDA_OK(cudaMemsetAsync(I->ib_cnt.p, 0, sizeof(int32_t) * (k + 1), st));
+  CUDA_OK(cudaMemsetAsync(I->ib_cursor.p, 0, sizeof(int32_t) * (k + 1), st));
+  CUDA_OK(cudaMemsetAsync(I->ib_pc.p, 0, sizeof(int32_t) * (k + 1), st));
+  CUDA_OK(cudaMemsetAsync(I->ib_bad.p, 0, sizeof(int32_t), st));
+  if (r1 > r0) {
+    g_launches++;
+    home_histogram_kernel<<<grid_for(r1 - r0), 256, 0, st>>>(d_home, r0, r1, k, I->ib_cnt.p, I->ib_bad.p);
+  }
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, I->ib_cnt.p, I->ib_off.p, k + 1, st);
+  size_t tb2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, I->ib_pc.p, I->ib_poff.p, k + 1, st);
+  I->cub_tmp.ensure(std::max(tb, tb2));
+  cub::DeviceScan::ExclusiveSum(I->cub_tmp.p, tb, I->ib_cnt.p, I->ib_off.p, k + 1, st);
+  if (r1 > r0) {
+    g_launches++;
+    home_scatter_kernel<<<grid_for(r1 - r0), 256, 0, st>>>(d_home, r0, r1, k, I->ib_off.p,
+                                                            I->ib_cursor.p, I->ib_sorted.p);
+  }
+  g_launches++;
+  piece_count_kernel<<<grid_for(k), 256, 0, st>>>(I->ib_cnt.p, k, kPieceRows, I->ib_pc.p);
+  cub::DeviceScan::ExclusiveSum(I->cub_tmp.p, tb2, I->ib_pc.p, I->ib_poff.p, k + 1, st);
+  CUDA_OK(cudaGetLastError());
+  if (check) {
+    int32_t bad = 0;
+    CUDA_OK(cudaMemcpyAsync(&bad, I->ib_bad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (bad) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: allotment shape mismatch");
+  }
+}
+
+void build_index_scan(lbdd_b200_instance* I, int64_t rows, int64_t* d_M, cudaStream_t st,
+                      int32_t id_offset = 0) {
+  const int32_t k = static_cast<int32_t>(I->k);
+  const int nv = static_cast<int>((k + 3) / 4);
+  int V = 1;
+  while (V < 8 && (nv + V - 1) / V > 1024) V *= 2;
+  int threads = (nv + V - 1) / V;
+  threads = ((threads + 31) / 32) * 32;
+  const int64_t max_pieces = rows / kPieceRows + k + 1;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_pieces, I->num_sms * 16)));
+#define LAUNCH_SEG(VV)                                                                  \
+  g_launches++;                                                                         \
+  seg_argmin_kernel<VV, kPieceRows><<<blocks, threads, 0, st>>>(                        \
+      I->d_cm, I->pitch, k, I->ib_sorted.p, I->ib_off.p, I->ib_cnt.p, I->ib_poff.p, d_M, id_offset)
+  switch (V) {
+    case 1: LAUNCH_SEG(1); break;
+    case 2: LAUNCH_SEG(2); break;
+    case 4: LAUNCH_SEG(4); break;
+    default: LAUNCH_SEG(8); break;
+  }
+#undef LAUNCH_SEG
+  CUDA_OK(cudaGetLastError());
+}
+
+void build_index_device(lbdd_b200_instance* I, const int32_t* d_home, int64_t r0, int64_t r1,
+                        int64_t* d_M, cudaStream_t st) {
+  build_index_prepare(I, d_home, r0, r1, st, true);
+  build_index_scan(I, r1 - r0, d_M, st);
+}
+
+// Assignment-cost sum + loads on the device, penalties on the host
+// (evaluate_partial_objective, core.hpp:216-233). Returns objective; fills
+// `loads` (k) and `missing`.
+int64_t device_objective(lbdd_b200_instance* I, const int32_t* d_home, std::vector<int64_t>& loads,
+                         int32_t* missing) {
+  const int64_t k = I->k;
+  I->obj_acc.ensure(k + 1);
+  I->obj_missing.ensure(1);
+  CUDA_OK(cudaMemsetAsync(I->obj_acc.p, 0, sizeof(unsigned long long) * (k + 1), I->stream));
+  CUDA_OK(cudaMemsetAsync(I->obj_missing.p, 0, sizeof(int32_t), I->stream));
+  g_launches++;
+  objective_kernel<<<grid_for(I->n), 256, 0, I->stream>>>(
+      I->d_cm, I->pitch, I->n, static_cast<int32_t>(k), d_home, I->obj_acc.p, I->obj_acc.p + 1,
+      I->obj_missing.p);
+  CUDA_OK(cudaGetLastError());
+  std::vector<unsigned long long> acc(k + 1);
+  CUDA_OK(cudaMemcpyAsync(acc.data(), I->obj_acc.p, sizeof(unsigned long long) * (k + 1),
+                          cudaMemcpyDeviceToHost, I->stream));
+  CUDA_OK(cudaMemcpyAsync(missing, I->obj_missing.p, sizeof(int32_t), cudaMemcpyDeviceToHost, I->stream));
+  CUDA_OK(cudaStreamSynchronize(I->stream));
+  loads.assign(k, 0);
+  int64_t total = static_cast<int64_t>(acc[0]);
+  for (int64_t s = 0; s < k; ++s) {
+    loads[s] = static_cast<int64_t>(acc[s + 1]);
+    total = checked_add(total, I->pen_total(s, loads[s] - I->cap[s]));
+  }
+  return total;
+}
+
+// engine workspace + launch geometry
+struct Launch {
+  int grid = 1;
+  int block = kEngineThreads;
+  size_t smem = 0;
+  bool tile = false;
+};
+
+int geo_chunk(int rows, int ncols, int grid, int block) {
+  const int ncoltiles = (ncols + block - 1) / block;
+  int want = grid / ncoltiles;
+  if (want < 1) want = 1;
+  int chunk = (rows + want - 1) / want;
+  return chunk < 1 ? 1 : chunk;
+}
+
+// must match carve_smem (engine.cu)
+size_t smem_bytes(int k, int maxchunk, int block, bool tile) {
+  return sizeof(int64_t) * maxchunk + sizeof(int64_t) * 4 + sizeof(PathEdge) * (k + 1) +
+         3 * sizeof(int32_t) * (k + 2) + 2 * sizeof(int32_t) * block + sizeof(int32_t) * 8 +
+         sizeof(int64_t) * maxchunk + sizeof(int32_t) * maxchunk +
+         (tile ? sizeof(int32_t) * static_cast<size_t>(maxchunk) * block : 0) +
+         2 * static_cast<size_t>(maxchunk) + 16;
+}
+
+constexpr size_t kSmemBudget = 200 * 1024;
+
+template <typename K>
+Launch plan_launch(lbdd_b200_instance* I, K kernel, int rows, int ncols, bool allow_tile) {
+  Launch L;
+  L.block = std::min(kEngineThreads, std::max(128, ((ncols + 31) / 32) * 32));
+  int64_t want = (static_cast<int64_t>(rows) * ncols + 4095) / 4096;
+  want = std::max<int64_t>(1, std::min<int64_t>(want, I->num_sms));
+  L.grid = static_cast<int>(want);
+  for (;;) {
+    const int chunk = geo_chunk(rows, ncols, L.grid, L.block);
+    L.tile = allow_tile && smem_bytes(rows, chunk, L.block, true) <= kSmemBudget;
+    L.smem = smem_bytes(rows, chunk, L.block, L.tile);
+    CUDA_OK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(L.smem)));
+    int per_sm = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, L.block, L.smem));
+    if (per_sm >= 1 && L.grid <= per_sm * I->num_sms) return L;
+    if (per_sm < 1) raise(LBDD_ERR_CUDA, "lbdd_b200: engine kernel does not fit on an SM");
+    L.grid = per_sm * I->num_sms;
+  }
+}
+
+void ensure_engine(lbdd_b200_instance* I, int64_t k_nodes) {
+  const int64_t k = I->k;
+  const int64_t nodes = std::max<int64_t>(k + 1, k_nodes);
+  I->home.ensure(I->n);
+  I->load.ensure(k + 1);
+  I->M.ensure(k * k);
+  for (int s = 0; s < 2; ++s) {
+    for (int i = 0; i < 2; ++i) { I->D[s][i].ensure(nodes); I->P[s][i].ensure(nodes); }
+    for (int i = 0; i < 3; ++i) I->B[s][i].ensure(nodes);
+  }
+  I->colW.ensure(k + 1);
+  I->path.ensure(k + 1);
+  I->inv_cnt.ensure(k + 2);
+  I->inv_cols.ensure((k + 1) * k);
+  I->rowslot.ensure(k + 1);
+  I->src_list.ensure(k + 1);
+  I->ctl.ensure(1);
+  I->bar.ensure(1);
+  I->dumflag.ensure(k + 1);
+  I->dummies.ensure(k + 1);
+  I->single_out.ensure(2);
+  I->single_gain.ensure(1);
+  I->rowver.ensure(k + 1);
+}
+
+EngineArgs engine_args(lbdd_b200_instance* I) {
+  EngineArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.cm = I->d_cm;
+  A.pitch = I->pitch;
+  A.n = static_cast<int32_t>(I->n);
+  A.k = static_cast<int32_t>(I->k);
+  A.cap = I->d_cap;
+  A.pfam = I->d_fam;
+  A.poff = I->d_off;
+  A.ppar = I->d_par;
+  A.home = I->home.p;
+  A.load = I->load.p;
+  A.M = I->M.p;
+  for (int s = 0; s < 2; ++s) {
+    for (int i = 0; i < 2; ++i) { A.D[s][i] = I->D[s][i].p; A.P[s][i] = I->P[s][i].p; }
+    for (int i = 0; i < 3; ++i) A.B[s][i] = I->B[s][i].p;
+  }
+  A.colW = I->colW.p;
+  A.path = I->path.p;
+  A.inv_cnt = I->inv_cnt.p;
+  A.inv_cols = I->inv_cols.p;
+  A.rowslot = I->rowslot.p;
+  A.src_list = I->src_list.p;
+  A.ctl = I->ctl.p;
+  A.bar = I->bar.p;
+  A.single_out = I->single_out.p;
+  A.single_gain = I->single_gain.p;
+  A.rowver = I->rowver.p;
+  A.single_kind = -1;
+  return A;
+}
+
+// fresh engine state: empty allotment, empty index
+void reset_engine_state(lbdd_b200_instance* I, int64_t delta0) {
+  const int64_t k = I->k;
+  CUDA_OK(cudaMemsetAsync(I->home.p, 0xff, sizeof(int32_t) * I->n, I->stream));
+  CUDA_OK(cudaMemsetAsync(I->load.p, 0, sizeof(int64_t) * (k + 1), I->stream));
+  fill64(I, I->M.p, k * k, kEmpty);
+  CUDA_OK(cudaMemsetAsync(I->inv_cnt.p, 0, sizeof(int32_t) * (k + 2), I->stream));
+  CUDA_OK(cudaMemsetAsync(I->rowslot.p, 0xff, sizeof(int32_t) * (k + 1), I->stream));
+  CUDA_OK(cudaMemsetAsync(I->bar.p, 0, sizeof(GridBar), I->stream));
+  CUDA_OK(cudaMemsetAsync(I->rowver.p, 0, sizeof(int32_t) * (k + 1), I->stream));
+  EngineCtl ctl;
+  std::memset(&ctl, 0, sizeof(ctl));
+  ctl.delta = delta0;
+  CUDA_OK(cudaMemcpyAsync(I->ctl.p, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, I->stream));
+}
+
+void raise_engine_error(int32_t code) {
+  switch (code) {
+    case kErrNegCycleWitness: raise(LBDD_ERR_LOGIC, "lbdd: negative cycle witnessed in anchored graph");
+    case kErrPathNotSimple: raise(LBDD_ERR_LOGIC, "lbdd: lowest-cost path is not simple");
+    case kErrBrokenParent: raise(LBDD_ERR_LOGIC, "lbdd: broken parent chain");
+    case kErrPathSum: raise(LBDD_ERR_LOGIC, "lbdd: path cost does not match edge sum");
+    case kErrStaleTransfer: raise(LBDD_ERR_LOGIC, "lbdd: stale transfer edge");
+    case kErrPenaltyEdge: raise(LBDD_ERR_LOGIC, "lbdd: path must close with a penalty edge");
+    case kErrPlaceholder: raise(LBDD_ERR_LOGIC, "lbdd: placeholder transfer without surplus");
+    case kErrNoResidual: raise(LBDD_ERR_LOGIC, "lbdd: no residual capacity left");
+    case kErrAlreadyIndexed: raise(LBDD_ERR_LOGIC, "lbdd: demand already indexed");
+    case kErrOverflow: raise(LBDD_ERR_OVERFLOW, "lbdd: cost accumulator overflow");
+    case kErrInvariant: raise(LBDD_ERR_LOGIC, "lbdd: negative cycle survived refinement");
+    case kErrNegativeLoad: raise(LBDD_ERR_LOGIC, "lbdd: negative load");
+    case kErrNotOverloaded: raise(LBDD_ERR_LOGIC, "lbdd: path graph requires an overloaded anchor");
+    default: raise(LBDD_ERR_RUNTIME, "lbdd_b200: engine error " + std::to_string(code));
+  }
+}
+
+EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64_t a_end) {
+  const Launch L = plan_launch(I, asral_engine_kernel, static_cast<int>(I->k),
+                               static_cast<int>(I->k + 1), true);
+  A.tile_mode = L.tile ? 1 : 0;
+  uint8_t* dumflag = I->dumflag.p;
+  EngineCtl ctl;
+  const int64_t chunk = int64_t(1) << 16;
+  int64_t a = a_begin;
+  do {
+    A.a_begin = a;
+    A.a_end = std::min(a_end, a + chunk);
+    void* args[] = {&A, &dumflag};
+    g_launches++;
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(asral_engine_kernel), dim3(L.grid),
+                                        dim3(L.block), args, L.smem, I->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(&ctl, I->ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    if (ctl.error) raise_engine_error(ctl.error);
+    A.search_base = ctl.search_count;
+    a = A.a_end;
+  } while (a < a_end);
+  return ctl;
+}
+
+void fill_report_stats(lbdd_solve_report* r, const EngineCtl& c) {
+  r->cycle_refine_calls = c.cycle_refine_calls;
+  r->path_refine_calls = c.path_refine_calls;
+  r->negative_cycles_removed = c.negative_cycles_removed;
+  r->negative_paths_removed = c.negative_paths_removed;
+  r->refinement_gain = c.refinement_gain;
+  r->transfers_applied = c.transfers_applied;
+  r->invariant_checks = c.invariant_checks;
+  r->bellman_ford_ns = c.t_bf_ns;
+  r->index_update_ns = c.t_index_ns;
+  r->relax_rounds = c.relax_rounds;
+  r->grid_barriers = c.barriers;
+}
+
+// detail::finish_report (solver.hpp:110-129): completeness + recount.
+int64_t finish(lbdd_b200_instance* I, int64_t delta, std::vector<int64_t>& loads) {
+  int32_t missing = 0;
+  const int64_t recount = device_objective(I, I->home.p, loads, &missing);
+  if (missing) raise(LBDD_ERR_LOGIC, "lbdd: solver produced an incomplete allotment");
+  if (recount != delta) raise(LBDD_ERR_LOGIC, "lbdd: tracked objective diverged from recount");
+  return delta;
+}
+
+void copy_out(lbdd_b200_instance* I, const int32_t* d_assign, int32_t* assignment_out,
+              const std::vector<int64_t>& loads, int64_t* load_out) {
+  if (assignment_out) {
+    CUDA_OK(cudaMemcpyAsync(assignment_out, d_assign, sizeof(int32_t) * I->n,
+                            cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+  }
+  if (load_out) std::copy(loads.begin(), loads.end(), load_out);
+}
+
+// asral_solve (solver.hpp:133-170)
+void solve_asral(lbdd_b200_instance* I, const lbdd_solver_options* o, int32_t solver,
+                 lbdd_solve_report* rep, int32_t* assignment_out, int64_t* load_out) {
+  const int64_t start = now_ns();
+  validate_centers(I);
+  check_device_range(I);
+  rep->scan_ns = arrival_scan(I, true);
+  ensure_engine(I, 0);
+  reset_engine_state(I, 0);
+  EngineArgs A = engine_args(I);
+  A.mode = 0;
+  A.arr_keys = I->keys_sorted.p;
+  A.best_center = I->best_center.p;
+  A.fixpoint = o && o->refine_to_fixpoint;
+  A.check_invariants = o && o->check_invariants;
+  const EngineCtl ctl = run_engine(I, A, 0, I->n);
+  std::vector<int64_t> loads;
+  rep->objective = finish(I, ctl.delta, loads);
+  fill_report_stats(rep, ctl);
+  rep->solver = solver;
+  copy_out(I, I->home.p, assignment_out, loads, load_out);
+  rep->total_ns = now_ns() - start;
+}
+
+// greedy_solve (solver.hpp:172-189): every demand at its row minimum.
+void solve_greedy(lbdd_b200_instance* I, lbdd_solve_report* rep, int32_t* assignment_out,
+                  int64_t* load_out) {
+  const int64_t start = now_ns();
+  validate_centers(I);
+  rep->scan_ns = arrival_scan(I, true);
+  std::vector<int64_t> loads;
+  int32_t missing = 0;
+  rep->objective = device_objective(I, I->best_center.p, loads, &missing);
+  rep->solver = LBDD_SOLVER_GREEDY;
+  copy_out(I, I->best_center.p, assignment_out, loads, load_out);
+  rep->total_ns = now_ns() - start;
+}
+
+// strict_solve (solver.hpp:227-301) incl. augment_with_dummy_center.
+void solve_strict(lbdd_b200_instance* I0, const lbdd_solver_options* o,
+                  lbdd_solve_report* rep, int32_t* assignment_out, int64_t* load_out) {
+  const int64_t start = now_ns();
+  validate_centers(I0);
+  check_device_range(I0);
+  rep->scan_ns = arrival_scan(I0, true);
+  const int64_t total_cap = I0->total_capacity();
+  const bool excess = total_cap < I0->n;
+  lbdd_b200_instance* W = I0;
+  std::unique_ptr<lbdd_b200_instance> aug;
+  if (excess) {
+    const int64_t deficit = I0->n - total_cap;
+    if (I0->max_cost + 1 > INT32_MAX)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: overflow-center cost exceeds int32");
+    aug.reset(new_instance(I0->device, I0->n, I0->k + 1));
+    W = aug.get();
+    CUDA_OK(cudaMalloc(&W->d_cm, sizeof(int32_t) * W->n * W->pitch));
+    W->owns_cm = true;
+    g_launches++;
+    augment_kernel<<<grid_for(W->n * W->pitch), 256, 0, W->stream>>>(
+        I0->d_cm, I0->pitch, W->d_cm, W->pitch, W->n, static_cast<int32_t>(I0->k),
+        static_cast<int32_t>(I0->max_cost + 1));
+    CUDA_OK(cudaGetLastError());
+    std::vector<int64_t> cap = I0->cap, off = I0->off, par = I0->par;
+    std::vector<int32_t> fam = I0->fam;
+    cap.push_back(deficit);
+    fam.push_back(LBDD_PENALTY_CONSTANT);
+    par.push_back(1);
+    off.push_back(off.back() + 1);
+    lbdd_instance_desc d{W->n, W->k, nullptr, cap.data(), fam.data(), off.data(), par.data()};
+    upload_centers(W, &d);
+    CUDA_OK(cudaStreamSynchronize(W->stream));
+  }
+  const int64_t k = W->k;
+  const int64_t n = W->n;
+  if (o && o->strict_order && o->strict_order_len > 0 && o->strict_order_len != n)
+    raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: strict order must cover every demand");
+  ensure_engine(W, 0);
+  reset_engine_state(W, 0);
+  CUDA_OK(cudaMemcpyAsync(W->dummies.p, W->cap.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice,
+                          W->stream));
+  EngineArgs A = engine_args(W);
+  A.mode = 1;
+  A.dummies = W->dummies.p;
+  A.check_invariants = o && o->check_invariants;
+  if (o && o->strict_order && o->strict_order_len > 0) {
+    W->order.ensure(n);
+    CUDA_OK(cudaMemcpyAsync(W->order.p, o->strict_order, sizeof(int32_t) * n,
+                            cudaMemcpyHostToDevice, W->stream));
+    A.order = W->order.p;
+  }
+  const EngineCtl ctl = run_engine(W, A, 0, n);
+  // capacity / placeholder accounting (solver.hpp:279-289)
+  std::vector<int64_t> dummies(k);
+  CUDA_OK(cudaMemcpyAsync(dummies.data(), W->dummies.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost,
+                          W->stream));
+  std::vector<int64_t> loads;
+  const int64_t obj = finish(W, ctl.delta, loads);
+  for (int64_t s = 0; s < k; ++s) {
+    if (loads[s] > W->cap[s]) raise(LBDD_ERR_LOGIC, "lbdd: strict solve exceeded a capacity");
+    if (loads[s] + dummies[s] != W->cap[s])
+      raise(LBDD_ERR_LOGIC, "lbdd: placeholder accounting out of balance");
+  }
+  rep->objective = obj;
+  fill_report_stats(rep, ctl);
+  rep->solver = LBDD_SOLVER_STRICT;
+  if (excess) {
+    const int64_t deficit = I0->n - total_cap;
+    rep->strict_surcharge = checked_mul(deficit, I0->max_cost + 1);
+    rep->has_dummy_center = 1;
+    rep->objective -= rep->strict_surcharge;
+  }
+  copy_out(W, W->home.p, assignment_out, loads, load_out);
+  rep->total_ns = now_ns() - start;
+}
+
+// SolverState::from_allotment (solver.hpp:61-68) on the device: allotment,
+// index (full segmented-argmin scan) and running objective.
+int64_t state_from_allotment(lbdd_b200_instance* I, const int32_t* assignment) {
+  ensure_engine(I, 0);
+  reset_engine_state(I, 0);
+  CUDA_OK(cudaMemcpyAsync(I->home.p, assignment, sizeof(int32_t) * I->n, cudaMemcpyHostToDevice,
+                          I->stream));
+  build_index_device(I, I->home.p, 0, I->n, I->M.p, I->stream);
+  std::vector<int64_t> loads;
+  int32_t missing = 0;
+  const int64_t delta = device_objective(I, I->home.p, loads, &missing);
+  CUDA_OK(cudaMemcpyAsync(I->load.p, loads.data(), sizeof(int64_t) * I->k, cudaMemcpyHostToDevice,
+                          I->stream));
+  EngineCtl ctl;
+  std::memset(&ctl, 0, sizeof(ctl));
+  ctl.delta = delta;
+  CUDA_OK(cudaMemcpyAsync(I->ctl.p, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, I->stream));
+  CUDA_OK(cudaStreamSynchronize(I->stream));
+  return delta;
+}
+
+void run_single(lbdd_b200_instance* I, EngineArgs A) {
+  const Launch L = plan_launch(I, asral_engine_kernel, static_cast<int>(I->k),
+                               static_cast<int>(I->k + 1), true);
+  A.tile_mode = L.tile ? 1 : 0;
+  uint8_t* dumflag = I->dumflag.p;
+  void* args[] = {&A, &dumflag};
+  g_launches++;
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(asral_engine_kernel), dim3(L.grid),
+                                      dim3(L.block), args, L.smem, I->stream));
+  CUDA_OK(cudaGetLastError());
+  EngineCtl ctl;
+  CUDA_OK(cudaMemcpyAsync(&ctl, I->ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, I->stream));
+  CUDA_OK(cudaStreamSynchronize(I->stream));
+  if (ctl.error) raise_engine_error(ctl.error);
+}
+
+// dense anchored-graph helpers (lowest_cost_path / relax_round API)
+struct DenseCtx {
+  lbdd_b200_instance* I;
+  DevBuf<int64_t> W;
+  DevBuf<int32_t> out;
+};
+
+lbdd_b200_instance* g_dense_inst = nullptr;
+
+lbdd_b200_instance* dense_instance(int32_t node_count) {
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  if (g_dense_inst == nullptr || g_dense_inst->k + 1 < node_count || g_dense_inst->device != dev) {
+    delete g_dense_inst;
+    g_dense_inst = new_instance(dev, 1, node_count - 1);
+  }
+  return g_dense_inst;
+}
+
+void check_dense(int32_t node_count, const int64_t* w) {
+  if (node_count < 2 || node_count > 65535)
+    raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: node_count must be in [2, 65535]");
+  const int64_t m = static_cast<int64_t>(node_count - 1) * node_count;
+  for (int64_t i = 0; i < m; ++i) {
+    if (w[i] != kNoEdge && (w[i] > (int64_t(1) << 40) || w[i] < -(int64_t(1) << 40)))
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: edge weight exceeds the device range (2^40)");
+  }
+}
+
+}  // namespace capi_detail
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* lbdd_b200_version(void) { return "lbdd_b200 0.1.0 (sm_100a)"; }
+long long lbdd_b200_launch_count(void) { return g_launches.load(); }
+const char* lbdd_b200_last_error(void) { return g_err.c_str(); }
+
+int lbdd_b200_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+lbdd_status lbdd_b200_instance_create(const lbdd_instance_desc* desc, int device,
+                                      lbdd_b200_instance** out) {
+  return guarded([&] {
+    if (desc->n < 0 || desc->k < 0) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: cost matrix size mismatch");
+    std::unique_ptr<lbdd_b200_instance> I(new_instance(device, desc->n, desc->k));
+    const size_t bytes = sizeof(int32_t) * std::max<int64_t>(I->n * I->pitch, 1);
+    CUDA_OK(cudaMalloc(&I->d_cm, bytes));
+    I->owns_cm = true;
+    if (I->n > 0 && I->k > 0) {
+      CUDA_OK(cudaMemcpy2DAsync(I->d_cm, sizeof(int32_t) * I->pitch, desc->costs,
+                                sizeof(int32_t) * I->k, sizeof(int32_t) * I->k, I->n,
+                                cudaMemcpyHostToDevice, I->stream));
+    }
+    upload_centers(I.get(), desc);
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    *out = I.release();
+  });
+}
+
+lbdd_status lbdd_b200_instance_create_device(const lbdd_instance_desc* desc, const int32_t* d_costs,
+                                             int64_t pitch_elems, int device,
+                                             lbdd_b200_instance** out) {
+  return guarded([&] {
+    if (pitch_elems < desc->k || pitch_elems % 4 != 0)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: pitch must be >= k and a multiple of 4");
+    std::unique_ptr<lbdd_b200_instance> I(new_instance(device, desc->n, desc->k));
+    I->pitch = pitch_elems;
+    I->d_cm = const_cast<int32_t*>(d_costs);
+    I->owns_cm = false;
+    upload_centers(I.get(), desc);
+    *out = I.release();
+  });
+}
+
+lbdd_status lbdd_b200_instance_generate(int64_t n, int64_t k, double theta, int64_t pen_lo,
+                                        int64_t pen_hi, int32_t mixed_families,
+                                        double capacity_skew, uint64_t seed, int device,
+                                        lbdd_b200_instance** out) {
+  return guarded([&] {
+    if (n < 1 || k < 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: n and k must be >= 1");
+    if (theta <= 0.0) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: theta must be positive");
+    if (pen_lo < 1 || pen_hi < pen_lo) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: bad penalty range");
+    std::unique_ptr<lbdd_b200_instance> I(new_instance(device, n, k));
+    CUDA_OK(cudaMalloc(&I->d_cm, sizeof(int32_t) * n * I->pitch));
+    I->owns_cm = true;
+    // host RNG for the k centers (splitmix64 stream)
+    uint64_t st = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+    auto next = [&st]() {
+      uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return z ^ (z >> 31);
+    };
+    auto u01 = [&]() { return static_cast<double>(next() >> 11) * 0x1.0p-53; };
+    auto below = [&](uint64_t b) { return next() % b; };
+    std::vector<double2> centers(k);
+    for (auto& c : centers) c = make_double2(u01(), u01());
+    DevBuf<double2> dc;
+    dc.ensure(k);
+    CUDA_OK(cudaMemcpyAsync(dc.p, centers.data(), sizeof(double2) * k, cudaMemcpyHostToDevice, I->stream));
+    g_launches++;
+    generate_costs_kernel<<<I->num_sms * 8, 256, 0, I->stream>>>(I->d_cm, I->pitch, 0, n,
+                                                                static_cast<int32_t>(k), seed, dc.p);
+    CUDA_OK(cudaGetLastError());
+    // capacities: total round(theta*n), multinomial over centers with
+    // weight (s+1)^-skew (skew 0: uniform, instgen.hpp:267-271)
+    const int64_t total = static_cast<int64_t>(std::llround(theta * static_cast<double>(n)));
+    std::vector<double> w(k);
+    double wsum = 0;
+    for (int64_t s = 0; s < k; ++s) {
+      w[s] = capacity_skew > 0 ? std::pow(static_cast<double>(s + 1), -capacity_skew) : 1.0;
+      wsum += w[s];
+    }
+    std::vector<int64_t> cap(k, 0);
+    int64_t assigned = 0;
+    for (int64_t s = 0; s < k; ++s) {
+      cap[s] = static_cast<int64_t>(std::floor(static_cast<double>(total) * w[s] / wsum));
+      assigned += cap[s];
+    }
+    for (int64_t r = assigned; r < total; ++r) cap[below(k)]++;
+    if (capacity_skew > 0) {  // skewed capacities land on random centers
+      for (int64_t s = k - 1; s > 0; --s) std::swap(cap[s], cap[below(s + 1)]);
+    }
+    std::vector<int32_t> fam(k);
+    std::vector<int64_t> off(k + 1, 0), par;
+    for (int64_t s = 0; s < k; ++s) {
+      const int64_t base = pen_lo + static_cast<int64_t>(below(pen_hi - pen_lo + 1));
+      const int f = mixed_families ? static_cast<int>(below(3)) : 0;
+      fam[s] = f;
+      if (f == 0) {
+        par.push_back(base);
+      } else if (f == 1) {
+        par.push_back(base);
+        par.push_back(static_cast<int64_t>(below(6)));
+      } else {
+        int64_t v = base;
+        for (int t = 0; t < 4; ++t) {
+          par.push_back(v);
+          v += static_cast<int64_t>(below(8));
+        }
+      }
+      off[s + 1] = static_cast<int64_t>(par.size());
+    }
+    lbdd_instance_desc d{n, k, nullptr, cap.data(), fam.data(), off.data(), par.data()};
+    upload_centers(I.get(), &d);
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    dc.release();
+    *out = I.release();
+  });
+}
+
+lbdd_status lbdd_b200_instance_destroy(lbdd_b200_instance* inst) {
+  return guarded([&] { delete inst; });
+}
+
+lbdd_status lbdd_b200_instance_shape(const lbdd_b200_instance* inst, int64_t* n, int64_t* k) {
+  return guarded([&] {
+    *n = inst->n;
+    *k = inst->k;
+  });
+}
+
+lbdd_status lbdd_b200_instance_centers(const lbdd_b200_instance* inst, int64_t* capacity,
+                                       int32_t* family, int64_t* offset, int64_t* params,
+                                       int64_t* n_params) {
+  return guarded([&] {
+    *n_params = static_cast<int64_t>(inst->par.size());
+    if (capacity) std::copy(inst->cap.begin(), inst->cap.end(), capacity);
+    if (family) std::copy(inst->fam.begin(), inst->fam.end(), family);
+    if (offset) std::copy(inst->off.begin(), inst->off.end(), offset);
+    if (params) std::copy(inst->par.begin(), inst->par.end(), params);
+  });
+}
+
+lbdd_status lbdd_b200_instance_costs(const lbdd_b200_instance* inst, int64_t row0, int64_t rows,
+                                     int32_t* out) {
+  return guarded([&] {
+    if (row0 < 0 || rows < 0 || row0 + rows > inst->n)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: row range out of bounds");
+    CUDA_OK(cudaSetDevice(inst->device));
+    CUDA_OK(cudaMemcpy2D(out, sizeof(int32_t) * inst->k, inst->d_cm + row0 * inst->pitch,
+                         sizeof(int32_t) * inst->pitch, sizeof(int32_t) * inst->k, rows,
+                         cudaMemcpyDeviceToHost));
+  });
+}
+
+lbdd_status lbdd_b200_solve(lbdd_b200_instance* inst, int32_t solver,
+                            const lbdd_solver_options* opts, lbdd_solve_report* report,
+                            int32_t* assignment_out, int64_t* load_out) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    std::memset(report, 0, sizeof(*report));
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    CUDA_OK(cudaEventRecord(e0, inst->stream));
+    switch (solver) {
+      case LBDD_SOLVER_ASRAL:
+      case LBDD_SOLVER_PARA_ASRAL:
+        solve_asral(inst, opts, solver, report, assignment_out, load_out);
+        break;
+      case LBDD_SOLVER_STRICT: solve_strict(inst, opts, report, assignment_out, load_out); break;
+      case LBDD_SOLVER_GREEDY: solve_greedy(inst, report, assignment_out, load_out); break;
+      default: raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: unknown solver");
+    }
+    CUDA_OK(cudaEventRecord(e1, inst->stream));
+    CUDA_OK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+    report->device_ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+lbdd_status lbdd_b200_build_index(lbdd_b200_instance* inst, const int32_t* assignment, int64_t row0,
+                                  int64_t rows, int64_t* min_transfer_out) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    if (rows < 0) { row0 = 0; rows = inst->n; }
+    if (row0 < 0 || row0 + rows > inst->n)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: row range out of bounds");
+    inst->home.ensure(inst->n);
+    inst->M.ensure(inst->k * inst->k);
+    CUDA_OK(cudaMemcpyAsync(inst->home.p, assignment, sizeof(int32_t) * inst->n,
+                            cudaMemcpyHostToDevice, inst->stream));
+    fill64(inst, inst->M.p, inst->k * inst->k, kEmpty);
+    build_index_device(inst, inst->home.p, row0, row0 + rows, inst->M.p, inst->stream);
+    CUDA_OK(cudaMemcpyAsync(min_transfer_out, inst->M.p, sizeof(int64_t) * inst->k * inst->k,
+                            cudaMemcpyDeviceToHost, inst->stream));
+    CUDA_OK(cudaStreamSynchronize(inst->stream));
+  });
+}
+
+lbdd_status lbdd_b200_build_index_device(lbdd_b200_instance* inst, const int32_t* d_assignment,
+                                         int64_t row0, int64_t rows, int64_t* d_out,
+                                         void* stream) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    if (rows < 0) { row0 = 0; rows = inst->n; }
+    if (row0 < 0 || row0 + rows > inst->n)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: row range out of bounds");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    g_launches++;
+    fill_i64_kernel<<<grid_for(inst->k * inst->k), 256, 0, st>>>(d_out, inst->k * inst->k, kEmpty);
+    CUDA_OK(cudaGetLastError());
+    build_index_device(inst, d_assignment, row0, row0 + rows, d_out, st);
+  });
+}
+
+lbdd_status lbdd_b200_build_index_shard(lbdd_b200_instance* inst, const int32_t* d_assignment,
+                                        int64_t demand_offset, int64_t* d_out, void* stream) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    if (demand_offset < 0 || demand_offset + inst->n >= INT32_MAX)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: demand ids exceed int32");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    g_launches++;
+    fill_i64_kernel<<<grid_for(inst->k * inst->k), 256, 0, st>>>(d_out, inst->k * inst->k, kEmpty);
+    CUDA_OK(cudaGetLastError());
+    build_index_prepare(inst, d_assignment, 0, inst->n, st, true);
+    build_index_scan(inst, inst->n, d_out, st, static_cast<int32_t>(demand_offset));
+  });
+}
+
+lbdd_status lbdd_b200_arrival_queue(lbdd_b200_instance* inst, int32_t* best_center,
+                                    int64_t* best_cost, int32_t* order) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    arrival_scan(inst, false);
+    std::vector<int64_t> sorted(inst->n);
+    CUDA_OK(cudaMemcpy(sorted.data(), inst->keys_sorted.p, sizeof(int64_t) * inst->n,
+                       cudaMemcpyDeviceToHost));
+    std::vector<int32_t> bc(inst->n);
+    CUDA_OK(cudaMemcpy(bc.data(), inst->best_center.p, sizeof(int32_t) * inst->n,
+                       cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < inst->n; ++i) {
+      const int32_t d = static_cast<int32_t>(sorted[i] & 0xffffffffLL);
+      if (order) order[i] = d;
+      if (best_cost) best_cost[d] = sorted[i] >> 32;
+    }
+    if (best_center) std::copy(bc.begin(), bc.end(), best_center);
+  });
+}
+
+lbdd_status lbdd_b200_refine(lbdd_b200_instance* inst, int32_t kind, int32_t anchor,
+                             int32_t* assignment, int64_t* dummies, int32_t* applied,
+                             int64_t* gain) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    if (kind != 0 && kind != 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: refine kind is 0 or 1");
+    if (anchor < 0 || anchor >= inst->k) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: bad anchor");
+    check_device_range(inst);
+    state_from_allotment(inst, assignment);
+    EngineArgs A = engine_args(inst);
+    A.single_kind = kind;
+    A.single_anchor = anchor;
+    if (dummies) {
+      CUDA_OK(cudaMemcpyAsync(inst->dummies.p, dummies, sizeof(int64_t) * inst->k,
+                              cudaMemcpyHostToDevice, inst->stream));
+      A.mode = 1;
+      A.dummies = inst->dummies.p;
+    }
+    run_single(inst, A);
+    int32_t out[2];
+    CUDA_OK(cudaMemcpy(out, inst->single_out.p, sizeof(out), cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(gain, inst->single_gain.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    *applied = out[0];
+    CUDA_OK(cudaMemcpy(assignment, inst->home.p, sizeof(int32_t) * inst->n, cudaMemcpyDeviceToHost));
+    if (dummies) {
+      CUDA_OK(cudaMemcpy(dummies, inst->dummies.p, sizeof(int64_t) * inst->k, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+lbdd_status lbdd_b200_gamma_has_negative_cycle(lbdd_b200_instance* inst, const int32_t* assignment,
+                                               const int64_t* dummies, int32_t* has_cycle) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    check_device_range(inst);
+    state_from_allotment(inst, assignment);
+    EngineArgs A = engine_args(inst);
+    A.single_kind = kGammaGraph;
+    if (dummies) {
+      CUDA_OK(cudaMemcpyAsync(inst->dummies.p, dummies, sizeof(int64_t) * inst->k,
+                              cudaMemcpyHostToDevice, inst->stream));
+      A.mode = 1;
+      A.dummies = inst->dummies.p;
+    }
+    run_single(inst, A);
+    int32_t out[2];
+    CUDA_OK(cudaMemcpy(out, inst->single_out.p, sizeof(out), cudaMemcpyDeviceToHost));
+    *has_cycle = out[0];
+  });
+}
+
+lbdd_status lbdd_b200_evaluate_objective(lbdd_b200_instance* inst, const int32_t* assignment,
+                                         int32_t partial, int64_t* objective) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    inst->home.ensure(inst->n);
+    for (int64_t d = 0; d < inst->n; ++d) {
+      if (assignment[d] < -1 || assignment[d] >= inst->k)
+        raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: allotment shape mismatch");
+    }
+    CUDA_OK(cudaMemcpyAsync(inst->home.p, assignment, sizeof(int32_t) * inst->n,
+                            cudaMemcpyHostToDevice, inst->stream));
+    std::vector<int64_t> loads;
+    int32_t missing = 0;
+    const int64_t v = device_objective(inst, inst->home.p, loads, &missing);
+    if (missing && !partial)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: objective of incomplete allotment");
+    *objective = v;
+  });
+}
+
+lbdd_status lbdd_b200_lowest_cost_path(int32_t node_count, int32_t anchor, const int64_t* weights,
+                                       int32_t* found, int64_t* cost, int64_t* dist,
+                                       int32_t* parent_node, int32_t* path, int32_t* path_len) {
+  return guarded([&] {
+    check_dense(node_count, weights);
+    if (anchor < 0 || anchor >= node_count - 1)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: bad anchor");
+    lbdd_b200_instance* I = dense_instance(node_count);
+    // the dense graph's "k" is rows; engine buffers sized for k+1 nodes
+    const int64_t saved_k = I->k;
+    I->k = node_count - 1;
+    ensure_engine(I, node_count);
+    DevBuf<int64_t> W;
+    DevBuf<int32_t> out;
+    const int64_t m = static_cast<int64_t>(node_count - 1) * node_count;
+    W.ensure(m);
+    out.ensure(1);
+    CUDA_OK(cudaMemcpyAsync(W.p, weights, sizeof(int64_t) * m, cudaMemcpyHostToDevice, I->stream));
+    CUDA_OK(cudaMemsetAsync(I->bar.p, 0, sizeof(GridBar), I->stream));
+    CUDA_OK(cudaMemsetAsync(I->ctl.p, 0, sizeof(EngineCtl), I->stream));
+    EngineArgs A = engine_args(I);
+    const Launch L = plan_launch(I, dense_path_kernel, node_count - 1, node_count, false);
+    int32_t one = 0;
+    const int64_t* wp = W.p;
+    int32_t* op = out.p;
+    void* args[] = {&A, &wp, &node_count, &anchor, &one, &op};
+    g_launches++;
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dense_path_kernel), dim3(L.grid),
+                                        dim3(L.block), args, L.smem, I->stream));
+    CUDA_OK(cudaGetLastError());
+    int32_t r = 0;
+    CUDA_OK(cudaMemcpyAsync(&r, out.p, sizeof(int32_t), cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    I->k = saved_k;
+    if (r < 0) raise(LBDD_ERR_LOGIC, "lbdd: negative cycle witnessed in anchored graph");
+    std::vector<int64_t> d(node_count);
+    std::vector<int32_t> p(node_count);
+    CUDA_OK(cudaMemcpy(d.data(), I->D[0][(r + 1) & 1].p, sizeof(int64_t) * node_count,
+                       cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(p.data(), I->P[0][(r + 1) & 1].p, sizeof(int32_t) * node_count,
+                       cudaMemcpyDeviceToHost));
+    *path_len = 0;
+    const int32_t sink = node_count - 1;
+    if (d[sink] >= kUnreachable) {
+      *found = 0;
+      return;
+    }
+    *found = 1;
+    *cost = d[sink];
+    std::copy(d.begin(), d.end(), dist);
+    std::copy(p.begin(), p.end(), parent_node);
+    // parent walk, refine.hpp:61-80
+    std::vector<int32_t> rev{sink};
+    std::vector<char> seen(node_count, 0);
+    int32_t node = sink;
+    while (node != anchor) {
+      if (seen[node]) raise(LBDD_ERR_LOGIC, "lbdd: lowest-cost path is not simple");
+      seen[node] = 1;
+      const int32_t u = p[node];
+      if (u < 0) raise(LBDD_ERR_LOGIC, "lbdd: broken parent chain");
+      rev.push_back(u);
+      node = u;
+    }
+    int64_t sum = 0;
+    const int32_t len = static_cast<int32_t>(rev.size()) - 1;
+    for (int32_t i = 0; i <= len; ++i) path[i] = rev[len - i];
+    for (int32_t i = 0; i < len; ++i) {
+      sum = checked_add(sum, weights[static_cast<int64_t>(path[i]) * node_count + path[i + 1]]);
+    }
+    if (sum != *cost) raise(LBDD_ERR_LOGIC, "lbdd: path cost does not match edge sum");
+    *path_len = len;
+  });
+}
+
+lbdd_status lbdd_b200_relax_round(int32_t node_count, const int64_t* weights,
+                                  const int64_t* dist_in, const int32_t* parent_in,
+                                  int64_t* dist_out, int32_t* parent_out, int32_t* changed) {
+  return guarded([&] {
+    check_dense(node_count, weights);
+    lbdd_b200_instance* I = dense_instance(node_count);
+    const int64_t saved_k = I->k;
+    I->k = node_count - 1;
+    ensure_engine(I, node_count);
+    DevBuf<int64_t> W;
+    DevBuf<int32_t> out;
+    const int64_t m = static_cast<int64_t>(node_count - 1) * node_count;
+    W.ensure(m);
+    out.ensure(1);
+    CUDA_OK(cudaMemcpyAsync(W.p, weights, sizeof(int64_t) * m, cudaMemcpyHostToDevice, I->stream));
+    CUDA_OK(cudaMemcpyAsync(I->D[0][1].p, dist_in, sizeof(int64_t) * node_count, cudaMemcpyHostToDevice, I->stream));
+    CUDA_OK(cudaMemcpyAsync(I->P[0][1].p, parent_in, sizeof(int32_t) * node_count, cudaMemcpyHostToDevice, I->stream));
+    fill64(I, I->B[0][0].p, node_count, kEmpty);
+    fill64(I, I->B[0][1].p, node_count, kEmpty);
+    CUDA_OK(cudaMemsetAsync(I->bar.p, 0, sizeof(GridBar), I->stream));
+    CUDA_OK(cudaMemsetAsync(I->ctl.p, 0, sizeof(EngineCtl), I->stream));
+    EngineArgs A = engine_args(I);
+    const Launch L = plan_launch(I, dense_path_kernel, node_count - 1, node_count, false);
+    int32_t one = 1;
+    int32_t anchor = -1;
+    const int64_t* wp = W.p;
+    int32_t* op = out.p;
+    void* args[] = {&A, &wp, &node_count, &anchor, &one, &op};
+    g_launches++;
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dense_path_kernel), dim3(L.grid),
+                                        dim3(L.block), args, L.smem, I->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(changed, out.p, sizeof(int32_t), cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaMemcpyAsync(dist_out, I->D[0][1].p, sizeof(int64_t) * node_count, cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaMemcpyAsync(parent_out, I->P[0][1].p, sizeof(int32_t) * node_count, cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    I->k = saved_k;
+  });
+}
+
+lbdd_status lbdd_b200_bench_index_scan(lbdd_b200_instance* inst, int32_t iters, double* mean_ms,
+                                       double* bytes_per_scan) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    if (!inst->scanned) arrival_scan(inst, false);
+    inst->M.ensure(inst->k * inst->k);
+    // warm-up (also sizes every scratch buffer)
+    fill64(inst, inst->M.p, inst->k * inst->k, kEmpty);
+    build_index_device(inst, inst->best_center.p, 0, inst->n, inst->M.p, inst->stream);
+    CUDA_OK(cudaStreamSynchronize(inst->stream));
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    double total = 0;
+    build_index_prepare(inst, inst->best_center.p, 0, inst->n, inst->stream, true);
+    for (int i = 0; i < iters; ++i) {
+      fill64(inst, inst->M.p, inst->k * inst->k, kEmpty);
+      CUDA_OK(cudaEventRecord(e0, inst->stream));
+      build_index_scan(inst, inst->n, inst->M.p, inst->stream);
+      CUDA_OK(cudaEventRecord(e1, inst->stream));
+      CUDA_OK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *mean_ms = total / std::max(iters, 1);
+    *bytes_per_scan = static_cast<double>(inst->n) * inst->k * 4.0 +
+                      static_cast<double>(inst->n) * 12.0 +
+                      static_cast<double>(inst->k) * inst->k * 8.0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+"""Parity of the B200 path (through the C ABI) with the oracle / reference
+fixtures. Integer work: every comparison is bit-exact."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import instance_from_json, load_golden
+import pyoracle as po
+from paper_2304_06543_b200.instance import PenaltySpec, ProblemInstance, ServiceCenter, SolverOptions
+from paper_2304_06543_b200 import LbddInvalidArgument, LbddLogicError
+from test_oracle_pinning import column_instance, worked_cycle_instance, worked_path_instance
+
+pytestmark = pytest.mark.gpu
+
+
+def same_report(a, b):
+    return (a.objective == b.objective and (np.asarray(a.assignment) == np.asarray(b.assignment)).all()
+            and a.stats == b.stats and a.strict_surcharge == b.strict_surcharge
+            and a.has_dummy_center == b.has_dummy_center and (np.asarray(a.load) == np.asarray(b.load)).all())
+
+
+def test_known_answers(dev):
+    assert dev.asral_solve(column_instance([4], 1, 10)).objective == 4
+    r = dev.asral_solve(column_instance([4, 6], 1, 10))
+    assert r.objective == 20 and r.stats.negative_cycles_removed == 0
+    r = dev.strict_solve(column_instance([2, 3, 4], 1, 10))
+    assert (r.objective, r.strict_surcharge, r.has_dummy_center) == (2, 10, True)
+    assert list(r.assignment) == [0, 1, 1]
+    with pytest.raises(LbddInvalidArgument):
+        dev.asral_solve(column_instance([0], 1, 10))
+
+
+def test_worked_examples(dev, oracle):
+    applied, gain, a, _ = dev.negative_cycle_refine(worked_cycle_instance(), [0, 1, 2, 3], 0)
+    assert applied and gain == -13
+    assert list(a) == list(oracle.refine(worked_cycle_instance(), 0, 0, [0, 1, 2, 3])[2])
+    applied, gain, a, _ = dev.negative_path_refine(worked_path_instance(), [0, 1, 2, 3, 0], 0)
+    assert applied and gain == -33
+    assert np.bincount(a, minlength=4).tolist() == [1, 1, 1, 2]
+    with pytest.raises(LbddLogicError):
+        dev.negative_path_refine(worked_cycle_instance(), [0, -1, -1, -1], 0)
+
+
+def random_graph(rng, k):
+    w = np.full((k, k + 1), po.NO_EDGE, np.int64)
+    anchor = rng() % k
+    for u in range(k):
+        for v in range(k):
+            if u != v and rng() % 10 < 6:
+                w[u, k if v == anchor else v] = (rng() % 41) - 20
+    return w, anchor
+
+
+def test_lowest_cost_path_matches_oracle(dev, oracle):
+    rng = po.Mt19937_64(43)
+    for _ in range(150):
+        w, anchor = random_graph(rng, 2 + rng() % 6)
+        try:
+            a = oracle.lowest_cost_path(w, anchor)
+        except LbddLogicError:
+            with pytest.raises(LbddLogicError):
+                dev.lowest_cost_path(w, anchor)
+            continue
+        b = dev.lowest_cost_path(w, anchor)
+        if a is None:
+            assert b is None
+            continue
+        assert a[0] == b[0]
+        assert (a[1] == b[1]).all() and (a[2] == b[2]).all() and (a[3] == b[3]).all()
+
+
+def test_relax_round_matches_oracle(dev, oracle):
+    rng = po.Mt19937_64(157)
+    for _ in range(100):
+        k = 2 + rng() % 6
+        w, anchor = random_graph(rng, k)
+        din = np.array([po.UNREACH if rng() % 4 == 0 else (rng() % 100) - 50 for _ in range(k + 1)])
+        din[anchor] = 0
+        pin = np.array([(rng() % (k + 1)) - 1 for _ in range(k + 1)], np.int32)
+        a = oracle.relax_round(w, din, pin)
+        b = dev.parallel_relax_round(w, din, pin)
+        assert a[0] == b[0] and (a[1] == b[1]).all() and (a[2] == b[2]).all()
+
+
+def test_build_index_and_gamma_match_oracle(dev, oracle):
+    rng = po.Mt19937_64(37)
+    for it in range(40):
+        n, k = 4 + rng() % 60, 1 + rng() % 7
+        inst = po.random_instance(rng, n=n, k=k)
+        asg = np.array([(rng() % (k + 1)) - 1 for _ in range(n)], np.int32)  # some unassigned
+        assert (dev.build_index(inst, asg) == oracle.build_index(inst, asg)).all()
+        full = np.array([rng() % k for _ in range(n)], np.int32)
+        assert dev.gamma_has_negative_cycle(inst, full) == oracle.gamma_has_negative_cycle(inst, full)
+        assert dev.evaluate_objective(inst, full) == oracle.evaluate_objective(inst, full)
+
+
+def test_refine_matches_oracle(dev, oracle):
+    rng = po.Mt19937_64(47)
+    for it in range(30):
+        n, k = 5 + rng() % 30, 2 + rng() % 4
+        inst = po.random_instance(rng, n=n, k=k)
+        asg = np.array([rng() % k for _ in range(n)], np.int32)
+        anchor = int(rng() % k)
+        a = oracle.refine(inst, 0, anchor, asg)
+        b = dev.negative_cycle_refine(inst, asg, anchor)
+        assert a[0] == b[0] and a[1] == b[1] and (a[2] == b[2]).all()
+        dm = np.array([rng() % 3 for _ in range(k)], np.int64)
+        a = oracle.refine(inst, 0, anchor, asg, dm)
+        b = dev.negative_cycle_refine(inst, asg, anchor, dm)
+        assert a[0] == b[0] and a[1] == b[1] and (a[2] == b[2]).all() and (a[3] == b[3]).all()
+
+
+def test_random_solves_match_reference_fixtures(dev):
+    for it, case in enumerate(load_golden("random_solves.json")):
+        inst = instance_from_json(case["instance"])
+        for key, gold in case["reports"].items():
+            solver, _, fix = key.partition("+")
+            rep = dev.solve(inst, solver, SolverOptions(refine_to_fixpoint=bool(fix),
+                                                        check_invariants=(it % 4 == 0)))
+            assert rep.objective == gold["objective"], key
+            assert rep.assignment.tolist() == gold["assignment"], key
+            assert rep.load.tolist() == gold["load"], key
+            assert rep.strict_surcharge == gold["strict_surcharge"], key
+            assert rep.stats.__dict__ == gold["stats"], key
+
+
+def test_road_graph_fixtures(dev):
+    for case in load_golden("road_graph.json"):
+        inst = instance_from_json(case["instance"])
+        for solver in ["asral", "strict"]:
+            rep = dev.solve(inst, solver)
+            assert rep.objective == case[solver]["objective"]
+            assert rep.assignment.tolist() == case[solver]["assignment"]
+
+
+def test_config0_matches_reference(dev, oracle):
+    """configs[0]: 10,000 x 100, theta 0.8 — bit-exact vs the reference."""
+    g = load_golden("config0.json")
+    inst = oracle.generate(g["seed"], g["n"], g["ratio"], g["theta"], *g["pen"])
+    for solver in ["greedy", "strict", "asral"]:
+        r = dev.solve(inst, solver)
+        gold = g["reports"][solver]
+        assert r.objective == gold["objective"], solver
+        assert hashlib.sha256(r.assignment.astype(np.int32).tobytes()).hexdigest() == \
+            gold["assignment_sha256"], solver
+        assert r.stats.__dict__ == gold["stats"], solver
+
+
+def test_fixpoint_parallel_and_order_options(dev, oracle):
+    rng = po.Mt19937_64(73)
+    for it in range(15):
+        n, k = 5 + rng() % 30, 2 + rng() % 4
+        inst = po.random_instance(rng, n=n, k=k, total_capacity=rng() % (n // 2 + 1))
+        for opts in [SolverOptions(refine_to_fixpoint=True), SolverOptions(parallel=True, workers=8)]:
+            assert same_report(dev.asral_solve(inst, opts), oracle.solve(inst, "asral", opts))
+        order = list(range(n))[::-1]
+        o = SolverOptions(strict_order=order)
+        assert same_report(dev.strict_solve(inst, o), oracle.solve(inst, "strict", o))
+
+
+def test_invariant_checking_counts(dev, oracle):
+    rng = po.Mt19937_64(71)
+    inst = po.random_instance(rng, n=40, k=5)
+    opts = SolverOptions(check_invariants=True)
+    a, b = dev.asral_solve(inst, opts), oracle.solve(inst, "asral", opts)
+    assert a.stats.invariant_checks == b.stats.invariant_checks > 0
+    assert same_report(a, b)

@@ -44,10 +44,20 @@ def test_product_does_not_reference_oracle():
                 assert "pyoracle" not in text and "lbdd_oracle" not in text, f
 
 
-def test_struct_layouts_match_header():
-    assert ctypes.sizeof(_abi.InstanceDesc) == 56
-    assert ctypes.sizeof(_abi.SolverOptionsC) == 48
-    assert ctypes.sizeof(_abi.SolveReportC) == 8 * 2 + 4 * 2 + 8 * 13
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors vs the C compiler's view of include/lbdd_b200.h."""
+    import subprocess
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "lbdd_b200.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu", sizeof(lbdd_instance_desc),'
+                   'sizeof(lbdd_solver_options), sizeof(lbdd_solve_report),'
+                   'offsetof(lbdd_solve_report, device_ns));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                            check=True).stdout.split()]
+    assert sizes == [ctypes.sizeof(_abi.InstanceDesc), ctypes.sizeof(_abi.SolverOptionsC),
+                     ctypes.sizeof(_abi.SolveReportC), _abi.SolveReportC.device_ns.offset]
 
 
 def test_penalty_semantics():  # core.hpp:60-95

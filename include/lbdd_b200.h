@@ -113,6 +113,11 @@ const char* lbdd_b200_last_error(void);
 int lbdd_b200_device_count(void);
 /* Kernels of this library launched so far in this process (all devices). */
 long long lbdd_b200_launch_count(void);
+/* Engine instrumentation of the last solve in this process: out[0..2]
+ * searches started (cycle, path, potential repair), out[3..5] of those with
+ * an empty initial frontier, out[6..8] frontier entries relaxed, out[9]
+ * path searches pruned by the penalty bound. */
+void lbdd_b200_engine_counters(int64_t* out);
 
 /* Upload an instance (host arrays) to `device`. Replaces constructing a
  * lbdd::ProblemInstance (core.hpp:130) — validation as in

@@ -11,6 +11,7 @@
 #include <memory>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 #include <stdexcept>
@@ -21,6 +22,7 @@
 #include "lbdd_b200.h"
 
 // Single translation unit: the kernels are included, not linked.
+#include "cluster.cu"
 #include "engine.cu"
 #include "scan.cu"
 
@@ -130,7 +132,9 @@ struct lbdd_b200_instance {
   DevBuf<int32_t> home, order, rowslot, src_list, inv_cnt, inv_cols, single_out, rowver;
   DevBuf<int32_t> P[2][2];
   DevBuf<int64_t> D[2][2], B[2][3];
-  DevBuf<int64_t> load, dummies, M, colW, single_gain;
+  DevBuf<int64_t> load, dummies, M, colW, single_gain, pi;
+  DevBuf<int32_t> dirty;
+  int cluster_size = 0;  // chosen once per instance
   DevBuf<EngineCtl> ctl;
   DevBuf<GridBar> bar;
   DevBuf<PathEdge> path;
@@ -155,6 +159,7 @@ struct lbdd_b200_instance {
       for (int i = 0; i < 3; ++i) B[s][i].release();
     }
     single_out.release(); rowver.release(); load.release(); dummies.release(); M.release();
+    pi.release(); dirty.release();
     colW.release();
     single_gain.release(); ctl.release(); bar.release(); path.release(); dumflag.release();
     ib_cnt.release(); ib_off.release(); ib_cursor.release(); ib_sorted.release();
@@ -524,6 +529,8 @@ void ensure_engine(lbdd_b200_instance* I, int64_t k_nodes) {
   I->single_out.ensure(2);
   I->single_gain.ensure(1);
   I->rowver.ensure(k + 1);
+  I->pi.ensure(k + 1);
+  I->dirty.ensure(static_cast<size_t>(16) * (2 * k + 4));
 }
 
 EngineArgs engine_args(lbdd_b200_instance* I) {
@@ -569,12 +576,14 @@ void reset_engine_state(lbdd_b200_instance* I, int64_t delta0) {
   CUDA_OK(cudaMemsetAsync(I->rowslot.p, 0xff, sizeof(int32_t) * (k + 1), I->stream));
   CUDA_OK(cudaMemsetAsync(I->bar.p, 0, sizeof(GridBar), I->stream));
   CUDA_OK(cudaMemsetAsync(I->rowver.p, 0, sizeof(int32_t) * (k + 1), I->stream));
+  CUDA_OK(cudaMemsetAsync(I->pi.p, 0, sizeof(int64_t) * (k + 1), I->stream));
   EngineCtl ctl;
   std::memset(&ctl, 0, sizeof(ctl));
   ctl.delta = delta0;
   CUDA_OK(cudaMemcpyAsync(I->ctl.p, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, I->stream));
 }
 
+int32_t g_err_arg = 0;
 void raise_engine_error(int32_t code) {
   switch (code) {
     case kErrNegCycleWitness: raise(LBDD_ERR_LOGIC, "lbdd: negative cycle witnessed in anchored graph");
@@ -590,7 +599,8 @@ void raise_engine_error(int32_t code) {
     case kErrInvariant: raise(LBDD_ERR_LOGIC, "lbdd: negative cycle survived refinement");
     case kErrNegativeLoad: raise(LBDD_ERR_LOGIC, "lbdd: negative load");
     case kErrNotOverloaded: raise(LBDD_ERR_LOGIC, "lbdd: path graph requires an overloaded anchor");
-    default: raise(LBDD_ERR_RUNTIME, "lbdd_b200: engine error " + std::to_string(code));
+    default: raise(LBDD_ERR_RUNTIME, "lbdd_b200: engine error " + std::to_string(code) +
+                   " arg " + std::to_string(g_err_arg));
   }
 }
 
@@ -619,7 +629,102 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
   return ctl;
 }
 
+// ---- the cluster engine (cluster.cu): one thread-block cluster ----
+size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
+  return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * s + 2 * sizeof(cl::Pub) + 8 * 16 +
+         sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::FEntry) * cl::kStage + 8 * (k + 1) +
+         4 * (cl::kMaxCS + 2) +
+         sizeof(PathEdge) * (k + 1) + 8 * block + 4 * 16 +
+         (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
+}
+
+bool use_grid_engine() {
+  const char* e = std::getenv("LBDD_B200_ENGINE");
+  return e != nullptr && std::string(e) == "grid";
+}
+
+// keys CM[d][v] - CM[d][u] fit the int16 tile when the cost range does
+bool keys_fit_int16(const lbdd_b200_instance* I) {
+  return I->scanned && I->min_cost >= 1 && I->max_cost + 1 - I->min_cost <= 32000;
+}
+
+EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64_t a_end,
+                             bool keys16) {
+  const int block = kEngineThreads;
+  const int k = static_cast<int>(I->k);
+  auto kernel = cluster_engine_kernel;
+  CUDA_OK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  cfg.blockDim = dim3(block);
+  cfg.stream = I->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (I->cluster_size == 0) {
+    for (int cs : {16, 8, 4, 2, 1}) {
+      const int s = (k + 1 + cs - 1) / cs;
+      const size_t smem = cluster_smem_bytes(k, s, block, false);
+      if (smem > 220 * 1024) continue;
+      CUDA_OK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+      cfg.gridDim = dim3(cs);
+      cfg.dynamicSmemBytes = smem;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kernel, &cfg) == cudaSuccess && nclusters > 0) {
+        I->cluster_size = cs;
+        break;
+      }
+      cudaGetLastError();
+    }
+    if (I->cluster_size == 0) raise(LBDD_ERR_CUDA, "lbdd_b200: no cluster configuration fits");
+  }
+  const int cs = I->cluster_size;
+  const int s = (k + 1 + cs - 1) / cs;
+  const bool tile = keys16 && cluster_smem_bytes(k, s, block, true) <= 220 * 1024;
+  A.tile_mode = tile ? 1 : 0;
+  const size_t smem = cluster_smem_bytes(k, s, block, tile);
+  CUDA_OK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  cfg.gridDim = dim3(cs);
+  cfg.dynamicSmemBytes = smem;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  EngineCtl ctl;
+  const int64_t chunk = int64_t(1) << 16;
+  int64_t a = a_begin;
+  int64_t* pi = I->pi.p;
+  int32_t* dirty = I->dirty.p;
+  do {
+    A.a_begin = a;
+    A.a_end = std::min(a_end, a + chunk);
+    g_launches++;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, A, pi, dirty));
+    CUDA_OK(cudaMemcpyAsync(&ctl, I->ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    g_err_arg = ctl.error_arg;
+    if (ctl.error) raise_engine_error(ctl.error);
+    a = A.a_end;
+  } while (a < a_end);
+  return ctl;
+}
+
+EngineCtl run_solver_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64_t a_end,
+                            bool keys16) {
+  const char* e = std::getenv("LBDD_B200_TILE");
+  if (e != nullptr && std::string(e) == "0") keys16 = false;
+  return use_grid_engine() ? run_engine(I, A, a_begin, a_end)
+                           : run_cluster_engine(I, A, a_begin, a_end, keys16);
+}
+
+EngineCtl g_last_ctl;  // instrumentation of the last engine run
+
 void fill_report_stats(lbdd_solve_report* r, const EngineCtl& c) {
+  g_last_ctl = c;
   r->cycle_refine_calls = c.cycle_refine_calls;
   r->path_refine_calls = c.path_refine_calls;
   r->negative_cycles_removed = c.negative_cycles_removed;
@@ -667,7 +772,7 @@ void solve_asral(lbdd_b200_instance* I, const lbdd_solver_options* o, int32_t so
   A.best_center = I->best_center.p;
   A.fixpoint = o && o->refine_to_fixpoint;
   A.check_invariants = o && o->check_invariants;
-  const EngineCtl ctl = run_engine(I, A, 0, I->n);
+  const EngineCtl ctl = run_solver_engine(I, A, 0, I->n, keys_fit_int16(I));
   std::vector<int64_t> loads;
   rep->objective = finish(I, ctl.delta, loads);
   fill_report_stats(rep, ctl);
@@ -742,7 +847,9 @@ void solve_strict(lbdd_b200_instance* I0, const lbdd_solver_options* o,
                             cudaMemcpyHostToDevice, W->stream));
     A.order = W->order.p;
   }
-  const EngineCtl ctl = run_engine(W, A, 0, n);
+  // augmented instance: the overflow column max+1 widens the range by one
+  const bool keys16 = keys_fit_int16(I0) && I0->max_cost + 2 - I0->min_cost <= 32000;
+  const EngineCtl ctl = run_solver_engine(W, A, 0, n, keys16);
   // capacity / placeholder accounting (solver.hpp:279-289)
   std::vector<int64_t> dummies(k);
   CUDA_OK(cudaMemcpyAsync(dummies.data(), W->dummies.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost,
@@ -843,6 +950,10 @@ extern "C" {
 
 const char* lbdd_b200_version(void) { return "lbdd_b200 0.1.0 (sm_100a)"; }
 long long lbdd_b200_launch_count(void) { return g_launches.load(); }
+/* Engine instrumentation of the last solve (16 counters, see cluster.cu). */
+void lbdd_b200_engine_counters(int64_t* out) {
+  for (int i = 0; i < 16; ++i) out[i] = g_last_ctl.dbg[i];
+}
 const char* lbdd_b200_last_error(void) { return g_err.c_str(); }
 
 int lbdd_b200_device_count(void) {

@@ -1,0 +1,990 @@
+// The cluster engine: the whole ASRAL / strict arrival loop on ONE thread-
+// block cluster (up to 16 CTAs on one GPC), synchronised with the hardware
+// cluster barrier and exchanging data through distributed shared memory.
+//
+// Exactness argument (DESIGN.md §3 has the long form):
+//  * The reference keeps the transfer graph Γ free of negative cycles
+//    (Lemmas 1-2; refine.hpp:125-131 checks it). So a feasible potential π
+//    exists: rc(u,v) = w(u,v) + π(u) - π(v) >= 0 on every Γ edge. We keep one,
+//    per center, in the owning CTA's shared memory.
+//  * After inserting demand d at anchor a only row a of Γ changed. In the
+//    anchored cycle graph every edge except those out of anchor-out has
+//    rc >= 0, so every prefix of a path with negative total cost is itself
+//    negative: searching only nodes reached with negative reduced distance
+//    finds every negative anchored path, with exact labels for every node on
+//    it (and for all their tight predecessors).
+//  * The reference's synchronous Bellman-Ford (parallel.hpp:145-169) leaves
+//    each node v with parent = the smallest u such that
+//    d*(u) + w(u,v) = d*(v) and h*(u) = h*(v) - 1, where h* is the fewest
+//    edges among shortest paths (the round in which d*(v) is first reached).
+//    Lexicographic labels (d, h) computed by ANY label-correcting order are
+//    unique, so a frontier search with packed (d << 16 | h) labels and the
+//    parent rule applied afterwards returns the reference's path bit for bit.
+//  * π is repaired after every change of Γ: D(v) = min(0, min_{x in X}
+//    dist_rc(x, v)) over the rows X that may now violate it (the anchor after
+//    an insert, the receiving centers of an applied path) is again a bounded
+//    negative-region search, and π + D is feasible.
+//  * The path search (overload) adds penalty edges u -> anchor-in whose
+//    reduced cost can be negative; nodes are explored while
+//    d_rc(v) < -min_u rc_pen(u), which bounds every candidate.
+//
+// Node ownership: node v (0..k, k = anchor-in) belongs to CTA v / s, s =
+// ceil((k+1)/CS); the owner holds its label, its π and its "changed" flag,
+// and relaxes every edge INTO its nodes, so label updates are CTA-local
+// shared-memory atomics. Sources of the next round are published as
+// (node, label, π, placeholder flag) lists read through DSMEM.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lbdd_b200 {
+namespace cl {
+
+constexpr int64_t kLabInf = INT64_MAX;
+constexpr int kMaxCS = 16;
+constexpr int kStage = 256;            // frontier entries staged per pass
+constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
+
+struct FEntry {
+  int32_t node;
+  int32_t dum;    // surplus placeholder at node (strict mode edge rule)
+  int64_t label;  // packed (d_rc << 16) + hops
+  int64_t pi;     // π(node)
+};
+
+struct Pub {          // per-CTA published scalars of one exchange
+  int32_t count;      // changed entries in list[par]
+  int32_t err;        // error recorded by this CTA
+  int64_t sinklab;    // label of anchor-in (owner only)
+  int64_t val;        // reduction slot (min over the CTA)
+  int32_t aux;        // reduction argument
+  int32_t pad;
+};
+
+struct CS {           // shared-memory layout of one CTA
+  int64_t* lab;       // [s]
+  int64_t* pis;       // [s]
+  FEntry* list[2];    // [s] each
+  Pub* pub[2];        // [1] each
+  PathEdge* path;     // [k + 1]
+  uint8_t* chg;       // [s]
+  int32_t* qd;        // [blockDim] rescan queue
+  int32_t* qs;        // [blockDim]
+  int32_t* misc;      // [16]: 0 queue count, 1 local count, 2 local err
+  int64_t* red;       // [16] reduction scratch
+  Pub* all;           // [kMaxCS] snapshot of every CTA's pub after a barrier
+  FEntry* stage;      // [kStage] frontier entries staged from DSMEM
+  int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
+  int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
+  int16_t* wt;        // [k * s] transfer keys of every row into my columns
+                      // (tile mode: all keys fit in int16)
+};
+
+// host mirror: cluster_smem_bytes() in capi.cu
+__device__ CS carve(unsigned char* p, int k, int s, bool tile) {
+  CS S;
+  S.lab = reinterpret_cast<int64_t*>(p); p += 8 * s;
+  S.pis = reinterpret_cast<int64_t*>(p); p += 8 * s;
+  S.list[0] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * s;
+  S.list[1] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * s;
+  S.pub[0] = reinterpret_cast<Pub*>(p); p += sizeof(Pub);
+  S.pub[1] = reinterpret_cast<Pub*>(p); p += sizeof(Pub);
+  S.red = reinterpret_cast<int64_t*>(p); p += 8 * 16;
+  S.all = reinterpret_cast<Pub*>(p); p += sizeof(Pub) * kMaxCS;
+  S.stage = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * kStage;
+  S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
+  S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
+  S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
+  S.qd = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
+  S.qs = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
+  S.misc = reinterpret_cast<int32_t*>(p); p += 4 * 16;
+  S.wt = reinterpret_cast<int16_t*>(p); p += tile ? 2 * static_cast<size_t>(k) * s : 0;
+  S.chg = reinterpret_cast<uint8_t*>(p);
+  return S;
+}
+
+__device__ __forceinline__ int64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<int64_t>(t);
+}
+__device__ __forceinline__ bool add_ovf(int64_t a, int64_t b, int64_t* r) {
+  const int64_t x = static_cast<int64_t>(static_cast<uint64_t>(a) + static_cast<uint64_t>(b));
+  *r = x;
+  return ((a ^ x) & (b ^ x)) < 0;
+}
+__device__ __forceinline__ bool mul_ovf(int64_t a, int64_t b, int64_t* r) {
+  const __int128 p = static_cast<__int128>(a) * static_cast<__int128>(b);
+  *r = static_cast<int64_t>(p);
+  return p != static_cast<__int128>(*r);
+}
+__device__ __forceinline__ int64_t pair_weight(int64_t m, bool dummy) {
+  if (dummy) {
+    if (m == kEmpty) return 0;
+    const int32_t key = transfer_key(m);
+    return key < 0 ? key : 0;
+  }
+  return m == kEmpty ? kNoEdge : static_cast<int64_t>(transfer_key(m));
+}
+__device__ __forceinline__ int32_t pair_kind(int64_t m, bool dummy) {
+  if (dummy && (m == kEmpty || transfer_key(m) >= 0)) return kEdgeDummy;
+  return m == kEmpty ? kEdgeNone : kEdgeTransfer;
+}
+__device__ __forceinline__ int64_t lab_d(int64_t lab) { return lab >> kCandShift; }
+__device__ __forceinline__ int16_t key16(int64_t m) {
+  return m == kEmpty ? kNoKey16 : static_cast<int16_t>(transfer_key(m));
+}
+__device__ __forceinline__ int64_t key16_weight(int16_t key, bool dummy) {
+  if (dummy) return key != kNoKey16 && key < 0 ? key : 0;
+  return key == kNoKey16 ? kNoEdge : static_cast<int64_t>(key);
+}
+__device__ __forceinline__ int32_t lab_h(int64_t lab) {
+  return static_cast<int32_t>(lab & ((int64_t(1) << kCandShift) - 1));
+}
+
+enum SearchKind : int32_t { kCycle = 0, kPath = 1, kRepair = 2 };
+
+struct Ctx {
+  EngineArgs A;
+  CS S;
+  cg::cluster_group cluster;
+  int rank, csz, k, s, v0, v1;
+  int par;
+  int err;            // sticky, identical in all CTAs (read at exchanges)
+  bool lead;          // rank 0, thread 0
+  bool tile;          // keys of my columns resident in S.wt
+  __device__ explicit Ctx(const cg::cluster_group& c) : cluster(c) {}
+};
+
+__device__ void set_err(Ctx& X, int code, int arg) {
+  if (atomicCAS(&X.A.ctl->error, 0, code) == 0) X.A.ctl->error_arg = arg;
+  X.S.misc[2] = 1;
+}
+
+// PenaltySpec::at / marginal / refund (core.hpp:60-74, 196-208)
+__device__ int64_t pen_at(Ctx& X, int s, int64_t j) {
+  const EngineArgs& A = X.A;
+  const int64_t* p = A.ppar + A.poff[s];
+  switch (A.pfam[s]) {
+    case 0: return p[0];
+    case 1: {
+      int64_t m, r;
+      if (mul_ovf(p[1], j - 1, &m) || add_ovf(p[0], m, &r)) { set_err(X, kErrOverflow, s); return 0; }
+      return r;
+    }
+    default: {
+      const int64_t len = A.poff[s + 1] - A.poff[s];
+      return p[(j < len ? j : len) - 1];
+    }
+  }
+}
+__device__ int64_t marginal_penalty(Ctx& X, int s, int64_t load) {
+  if (load < 0) { set_err(X, kErrNegativeLoad, s); return 0; }
+  return load < X.A.cap[s] ? 0 : pen_at(X, s, load - X.A.cap[s] + 1);
+}
+__device__ int64_t refund_penalty(Ctx& X, int s, int64_t load) {
+  if (load < 0) { set_err(X, kErrNegativeLoad, s); return 0; }
+  return load <= X.A.cap[s] ? 0 : pen_at(X, s, load - X.A.cap[s]);
+}
+
+__device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
+  return X.A.dummies != nullptr && X.A.dummies[u] > 0;
+}
+
+// Cluster barrier + exchange: every CTA publishes pub[par] (count, err,
+// sink label, reduction slot) — and list[par] — before calling; afterwards
+// S.all[] holds the values of every CTA, identical everywhere, and par
+// flips, so list[par ^ 1] are the sources of the next relaxation.
+__device__ void exchange(Ctx& X) {
+  if (threadIdx.x == 0) X.S.pub[X.par]->err = X.S.misc[2];
+  X.cluster.sync();
+  if (threadIdx.x < X.csz) {
+    const Pub* rp = X.cluster.map_shared_rank(X.S.pub[X.par], threadIdx.x);
+    X.S.all[threadIdx.x] = *rp;
+  }
+  if (X.lead) X.A.ctl->barriers += 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    X.S.pref[0] = 0;
+    for (int r = 0; r < X.csz; ++r) {
+      const int c = X.S.all[r].count;
+      acc += (c >= 0 && c <= X.s) ? c : 0;
+      X.S.pref[r + 1] = acc;
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < X.csz; ++r) X.err |= X.S.all[r].err;
+  // the next phase writes the other buffer while slow CTAs may still read
+  // this one; it is rewritten only after the next barrier
+  X.par ^= 1;
+}
+
+__device__ int total_count(const Ctx& X) {
+  int t = 0;
+  for (int r = 0; r < X.csz; ++r) t += X.S.all[r].count;
+  return t;
+}
+
+// Publish this CTA's changed nodes (and clear the flags) into list[par].
+__device__ void collect(Ctx& X, int kind, int anchor) {
+  CS& S = X.S;
+  if (threadIdx.x == 0) S.misc[1] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    if (!S.chg[i]) continue;
+    S.chg[i] = 0;
+    const int v = X.v0 + i;
+    if (v == X.k) continue;  // anchor-in has no out-edges
+    const int pos = atomicAdd(&S.misc[1], 1);
+    FEntry e;
+    e.node = v;
+    e.dum = (kind != kPath && has_dummy(X, v)) ? 1 : 0;
+    e.label = S.lab[i];
+    e.pi = S.pis[i];
+    S.list[X.par][pos] = e;
+    if (lab_h(e.label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Pub* p = S.pub[X.par];
+    p->count = S.misc[1];
+    p->sinklab = (X.k >= X.v0 && X.k < X.v1) ? S.lab[X.k - X.v0] : kLabInf;
+  }
+}
+
+// Relax every edge from the published sources of the last exchange into
+// this CTA's nodes. bound_mid / bound_sink: strict upper bounds on labels.
+// Sources are staged from DSMEM into shared memory; each thread owns one
+// destination column per pass and keeps its running minimum in a register,
+// so a column sees one shared-memory atomicMin per pass.
+__device__ void relax(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
+                      int64_t bound_sink) {
+  CS& S = X.S;
+  const EngineArgs& A = X.A;
+  const int ns = X.v1 - X.v0;
+  if (ns <= 0) return;  // uniform within the CTA
+  const int prev = X.par ^ 1;  // sources: the buffer of the last exchange
+  const int32_t* pref = S.pref;
+  const int total = pref[X.csz];
+  const int cpp = ns < static_cast<int>(blockDim.x) ? ((ns + 31) & ~31) : blockDim.x;
+  const int rpp = blockDim.x / cpp;
+  const int tx = threadIdx.x % cpp;
+  const int ty = threadIdx.x / cpp;
+  for (int g0 = 0; g0 < total; g0 += kStage) {
+    const int cnt = min(kStage, total - g0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const int g = g0 + t;
+      int r = 0;
+      while (g >= pref[r + 1]) ++r;
+      const FEntry* rl = X.cluster.map_shared_rank(S.list[prev], r);
+      FEntry e = rl[g - pref[r]];
+      if (e.node < 0 || e.node >= X.k) { set_err(X, 200, e.node); e.node = 0; e.label = kLabInf / 2; }
+      S.stage[t] = e;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < ns; c0 += cpp) {
+      const int col = c0 + tx;
+      const int v = X.v0 + col;
+      if (col >= ns || ty >= cnt) continue;
+      const bool sinkcol = kind != kRepair && v == X.k;
+      if (v > X.k || (kind != kRepair && v == anchor) || (kind == kRepair && v == X.k)) continue;
+      const int64_t piv = S.pis[col];
+      const int64_t bound = sinkcol ? bound_sink : bound_mid;
+      int64_t best = kLabInf;
+      if (sinkcol) {
+        for (int t = ty; t < cnt; t += rpp) {
+          const FEntry e = S.stage[t];
+          const int64_t w = S.sinkw[e.node];  // kNoEdge for the anchor itself
+          if (w == kNoEdge) continue;
+          const int64_t cand = e.label + (w + e.pi - piv) * (int64_t(1) << kCandShift) + 1;
+          if (cand < bound && cand < best) best = cand;
+        }
+      } else if (X.tile) {
+#pragma unroll 4
+        for (int t = ty; t < cnt; t += rpp) {
+          const FEntry e = S.stage[t];
+          const int64_t w = key16_weight(S.wt[static_cast<int64_t>(e.node) * X.s + col], e.dum != 0);
+          if (e.node == v || w == kNoEdge) continue;
+          const int64_t cand = e.label + (w + e.pi - piv) * (int64_t(1) << kCandShift) + 1;
+          if (cand < bound && cand < best) best = cand;
+        }
+      } else {
+        // keys from global memory, 4 independent loads in flight
+        for (int t = ty; t < cnt; t += 4 * rpp) {
+          int64_t m[4];
+          FEntry e[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int tq = t + q * rpp;
+            e[q].node = -1;
+            m[q] = kEmpty;
+            if (tq < cnt) {
+              e[q] = S.stage[tq];
+              m[q] = A.M[static_cast<int64_t>(e[q].node) * A.k + v];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (e[q].node < 0 || e[q].node == v) continue;
+            const int64_t w = pair_weight(m[q], e[q].dum != 0);
+            if (w == kNoEdge) continue;
+            const int64_t cand = e[q].label + (w + e[q].pi - piv) * (int64_t(1) << kCandShift) + 1;
+            if (cand < bound && cand < best) best = cand;
+          }
+        }
+      }
+      if (best != kLabInf) {
+        const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
+                                        static_cast<long long>(best));
+        if (best < old) S.chg[col] = 1;
+      }
+    }
+  }
+}
+
+// Weights of every edge into anchor-in, precomputed by its owner at the
+// start of a search: cycle graph w(u, anchor) (cheapest_pair_edge), path
+// graph the penalty difference marginal(u) - refund(anchor).
+__device__ void fill_sink_weights(Ctx& X, int kind, int anchor, int64_t refund_a) {
+  if (!(X.k >= X.v0 && X.k < X.v1)) return;
+  const EngineArgs& A = X.A;
+  for (int u = threadIdx.x; u < X.k; u += blockDim.x) {
+    int64_t w = kNoEdge;
+    if (u != anchor) {
+      w = kind == kCycle ? pair_weight(A.M[static_cast<int64_t>(u) * A.k + anchor], has_dummy(X, u))
+                         : marginal_penalty(X, u, A.load[u]) - refund_a;
+    }
+    X.S.sinkw[u] = w;
+  }
+}
+
+// Run rounds until no label changes. Sources must already be published in
+// list[par] (count in pub[par]) and exchanged. Returns rounds executed.
+__device__ int search_rounds(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
+                             int64_t bound_sink) {
+  int rounds = 0;
+  if (X.lead) {
+    X.A.ctl->dbg[kind] += 1;                   // searches started per kind
+    if (total_count(X) == 0) X.A.ctl->dbg[3 + kind] += 1;  // empty at start
+  }
+  while (total_count(X) > 0 && !X.err) {
+    if (X.lead) X.A.ctl->dbg[6 + kind] += total_count(X);  // frontier entries
+    relax(X, kind, anchor, refund_a, bound_mid, bound_sink);
+    __syncthreads();
+    collect(X, kind, anchor);
+    exchange(X);
+    ++rounds;
+  }
+  // explored nodes (finite labels), per kind
+  int loc = 0;
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) loc += X.S.lab[i] != kLabInf;
+  atomicAdd(reinterpret_cast<unsigned long long*>(&X.A.ctl->dbg[10 + kind]),
+            static_cast<unsigned long long>(loc));
+  return rounds;
+}
+
+__device__ int64_t sink_label(const Ctx& X) {
+  int64_t l = kLabInf;
+  for (int r = 0; r < X.csz; ++r) l = min(l, X.S.all[r].sinklab);
+  return l;
+}
+
+// Start a search: labels of owned nodes to +inf, π(anchor-in) := π(anchor).
+__device__ void reset_labels(Ctx& X, int64_t pi_anchor) {
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    X.S.lab[i] = kLabInf;
+    X.S.chg[i] = 0;
+    if (X.v0 + i == X.k) X.S.pis[i] = pi_anchor;
+  }
+}
+
+// Read π(v) of any node (DSMEM).
+__device__ int64_t pi_of(Ctx& X, int v) {
+  const int r = v / X.s;
+  const int64_t* rp = X.cluster.map_shared_rank(X.S.pis, r);
+  return rp[v - r * X.s];
+}
+
+// Publish a single source (label 0) owned by this CTA into list[par].
+__device__ void publish_sources(Ctx& X, const int* nodes, int count, int kind) {
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int i = 0; i < count; ++i) {
+      const int v = nodes[i];
+      if (v < X.v0 || v >= X.v1) continue;
+      bool dup = false;
+      for (int j = 0; j < i; ++j) dup |= nodes[j] == v;
+      if (dup) continue;
+      X.S.lab[v - X.v0] = 0;
+      FEntry e;
+      e.node = v;
+      e.dum = (kind != kPath && has_dummy(X, v)) ? 1 : 0;
+      e.label = 0;
+      e.pi = X.S.pis[v - X.v0];
+      X.S.list[X.par][c++] = e;
+    }
+    X.S.pub[X.par]->count = c;
+    X.S.pub[X.par]->sinklab = kLabInf;
+  }
+}
+
+// π(v) += min(0, d(v)) for owned nodes explored by the last search. Ends
+// with a cluster barrier: other CTAs read π through DSMEM (pi_of) next.
+__device__ void apply_repair(Ctx& X) {
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    if (X.v0 + i == X.k) continue;
+    const int64_t l = X.S.lab[i];
+    if (l == kLabInf) continue;
+    const int64_t d = lab_d(l);
+    if (d < 0) {
+      X.S.pis[i] += d;
+      if (X.S.pis[i] < -(int64_t(1) << 44)) set_err(X, kErrOverflow, X.v0 + i);
+    }
+  }
+  X.cluster.sync();
+}
+
+// Parent walk (refine.hpp:53-80) with the synchronous-BF parent rule:
+// parent(v) = min u with lab(u) + rc(u,v)*2^16 + 1 == lab(v). Fills S.path
+// (in path order) and returns its length; 0 + error on a broken chain.
+__device__ int reconstruct(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t sinklab) {
+  CS& S = X.S;
+  const EngineArgs& A = X.A;
+  int v = X.k;
+  int64_t lv = sinklab;
+  int64_t piv = pi_of(X, anchor);  // π(anchor-in) = π(anchor)
+  int len = 0;
+  while (v != anchor) {
+    if (len > X.k) { set_err(X, kErrPathNotSimple, len); break; }
+    // smallest owned explored u whose edge into v is tight
+    int64_t best = kEmpty;
+    for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+      const int u = X.v0 + i;
+      if (u == X.k || u == v) continue;
+      const int64_t lu = S.lab[i];
+      if (lu == kLabInf) continue;
+      int64_t w;
+      const bool dum = kind == kCycle && has_dummy(X, u);
+      if (v == X.k) {
+        if (u == anchor) continue;
+        w = kind == kCycle ? pair_weight(A.M[static_cast<int64_t>(u) * A.k + anchor], dum)
+                           : marginal_penalty(X, u, A.load[u]) - refund_a;
+      } else {
+        if (v == anchor) continue;
+        w = pair_weight(A.M[static_cast<int64_t>(u) * A.k + v], dum);
+      }
+      if (w == kNoEdge) continue;
+      const int64_t rc = w + S.pis[i] - piv;
+      if (lu + rc * (int64_t(1) << kCandShift) + 1 != lv) continue;
+      best = min(best, static_cast<int64_t>(u));
+    }
+    if (threadIdx.x == 0) S.red[0] = kEmpty;
+    __syncthreads();
+    atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(best));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Pub* p = S.pub[X.par];
+      const int64_t bu = S.red[0];
+      p->val = bu;
+      p->count = 0;
+      p->sinklab = bu == kEmpty ? kLabInf : S.lab[bu - X.v0];  // the parent's label
+    }
+    exchange(X);
+    int64_t u = kEmpty;
+    int64_t lu = 0;
+    for (int r = 0; r < X.csz; ++r) {
+      if (S.all[r].val < u) {
+        u = S.all[r].val;
+        lu = S.all[r].sinklab;
+      }
+    }
+    if (u == kEmpty) { set_err(X, kErrBrokenParent, v); X.err = 1; break; }
+    // record edge u -> v (reversed order for now)
+    if (threadIdx.x == 0) {
+      PathEdge e;
+      const int uu = static_cast<int>(u);
+      const int cv = v == X.k ? anchor : v;
+      e.from_center = uu;
+      e.to_center = cv;
+      e.demand = -1;
+      if (kind == kPath && v == X.k) {
+        e.kind = kEdgePenalty;
+      } else {
+        const int64_t m = A.M[static_cast<int64_t>(uu) * A.k + cv];
+        const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[uu] > 0;
+        e.kind = pair_kind(m, dum);
+        if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
+      }
+      S.path[len] = e;
+    }
+    piv = pi_of(X, static_cast<int>(u));
+    lv = lu;
+    v = static_cast<int>(u);
+    ++len;
+    __syncthreads();
+  }
+  // reverse into path order
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < len / 2; ++i) {
+      const PathEdge t = S.path[i];
+      S.path[i] = S.path[len - 1 - i];
+      S.path[len - 1 - i] = t;
+    }
+  }
+  __syncthreads();
+  return X.err ? 0 : len;
+}
+
+// Apply the path (apply_path_edges, refine.hpp:134-164). Column owners
+// invalidate and fold gains for their columns; the lead updates the
+// allotment; all CTAs rescan the invalidated entries over the final
+// buckets. Fills `dirty` with the rows whose out-edges may now violate π.
+__device__ int apply(Ctx& X, int kind, int len, int64_t cost, int* dirty) {
+  CS& S = X.S;
+  const EngineArgs& A = X.A;
+  const int k = X.k;
+  const int64_t t0 = gtimer();
+  // ---- T1: invalidate (owners) ----
+  const int jlo = X.v0, jhi = min(X.v1, k);
+  for (int i = 0; i < len; ++i) {
+    const PathEdge e = S.path[i];
+    if (e.kind != kEdgeTransfer) continue;
+    for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
+      if (j == e.from_center) continue;
+      int64_t* p = &A.M[static_cast<int64_t>(e.from_center) * k + j];
+      const int64_t m = *p;
+      if (m != kEmpty && transfer_demand(m) == e.demand) {
+        *p = kEmpty;
+        if (X.tile) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = kNoKey16;
+        const int pos = atomicAdd(&A.inv_cnt[i], 1);
+        A.inv_cols[static_cast<int64_t>(i) * k + pos] = j;
+      }
+    }
+  }
+  __syncthreads();
+  // gains into the receiving rows (same thread per column: after the clears)
+  for (int i = 0; i < len; ++i) {
+    const PathEdge e = S.path[i];
+    if (e.kind != kEdgeTransfer) continue;
+    const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+    const int32_t hv = row[e.to_center];
+    for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
+      if (j == e.to_center) continue;
+      int64_t* p = &A.M[static_cast<int64_t>(e.to_center) * k + j];
+      const int64_t v = pack_transfer(row[j] - hv, e.demand);
+      if (v < *p) {
+        *p = v;
+        if (X.tile) S.wt[static_cast<int64_t>(e.to_center) * X.s + (j - X.v0)] = key16(v);
+      }
+    }
+  }
+  int nd = 0;
+  for (int i = 0; i < len; ++i) {
+    const PathEdge e = S.path[i];
+    if (e.kind == kEdgeTransfer || e.kind == kEdgeDummy) dirty[nd++] = e.to_center;
+  }
+  if (X.lead) {
+    EngineCtl* ctl = A.ctl;
+    for (int i = 0; i < ctl->prev_sources; ++i) A.rowslot[A.src_list[i]] = -1;
+    int ns = 0;
+    for (int i = 0; i < len; ++i) {
+      const PathEdge e = S.path[i];
+      if (e.kind == kEdgeTransfer) {
+        if (A.home[e.demand] != e.from_center) { set_err(X, kErrStaleTransfer, e.demand); break; }
+        A.home[e.demand] = e.to_center;
+        A.load[e.from_center] -= 1;
+        A.load[e.to_center] += 1;
+        A.rowslot[e.from_center] = i;
+        A.src_list[ns++] = e.from_center;
+        ctl->transfers_applied += 1;
+      } else if (e.kind == kEdgeDummy) {
+        if (A.dummies == nullptr || A.dummies[e.from_center] <= 0) {
+          set_err(X, kErrPlaceholder, e.from_center);
+          break;
+        }
+        A.dummies[e.from_center] -= 1;
+        A.dummies[e.to_center] += 1;
+      } else if (e.kind == kEdgePenalty) {
+        if (i != len - 1) { set_err(X, kErrPenaltyEdge, i); break; }
+      }
+    }
+    ctl->prev_sources = ns;
+    int64_t r;
+    if (add_ovf(ctl->delta, cost, &r)) set_err(X, kErrOverflow, 0);
+    ctl->delta = r;
+    if (add_ovf(ctl->refinement_gain, -cost, &r)) set_err(X, kErrOverflow, 1);
+    ctl->refinement_gain = r;
+    if (kind == kCycle) ctl->negative_cycles_removed += 1;
+    else ctl->negative_paths_removed += 1;
+  }
+  if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+  exchange(X);
+  // ---- T3: rescans of the invalidated entries over the final buckets ----
+  int total = 0;
+  for (int i = 0; i < len; ++i) total += (S.path[i].kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
+  if (total > 0) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    const int64_t per = (A.n + X.csz - 1) / X.csz;
+    const int64_t b0 = per * X.rank;
+    const int64_t b1 = (b0 + per < A.n) ? b0 + per : A.n;
+    for (int64_t base = b0; base < b1; base += blockDim.x) {
+      if (threadIdx.x == 0) S.misc[0] = 0;
+      __syncthreads();
+      const int64_t d = base + threadIdx.x;
+      if (d < b1) {
+        const int32_t h = A.home[d];
+        if (h >= 0) {
+          const int32_t sl = A.rowslot[h];
+          if (sl >= 0 && A.inv_cnt[sl] > 0) {
+            const int q = atomicAdd(&S.misc[0], 1);
+            S.qd[q] = static_cast<int32_t>(d);
+            S.qs[q] = sl;
+          }
+        }
+      }
+      __syncthreads();
+      const int qn = S.misc[0];
+      for (int q = warp; q < qn; q += nw) {
+        const int32_t dd = S.qd[q];
+        const int sl = S.qs[q];
+        const int u = S.path[sl].from_center;
+        const int32_t* row = A.cm + static_cast<int64_t>(dd) * A.pitch;
+        const int32_t hv = row[u];
+        const int cnt = A.inv_cnt[sl];
+        const int32_t* cols = A.inv_cols + static_cast<int64_t>(sl) * k;
+        for (int x = lane; x < cnt; x += 32) {
+          const int j = cols[x];
+          atomicMin(reinterpret_cast<long long*>(&A.M[static_cast<int64_t>(u) * k + j]),
+                    static_cast<long long>(pack_transfer(row[j] - hv, dd)));
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+  exchange(X);
+  // rescans wrote M with atomics from every CTA: refresh my tile columns of
+  // the source rows
+  if (X.tile) {
+    for (int i = 0; i < len; ++i) {
+      const PathEdge e = S.path[i];
+      if (e.kind != kEdgeTransfer) continue;
+      for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
+        S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] =
+            key16(A.M[static_cast<int64_t>(e.from_center) * k + j]);
+      }
+    }
+    __syncthreads();
+  }
+  // counters for the next apply are reset before the next one starts
+  if (X.lead) {
+    for (int i = 0; i < len; ++i) A.inv_cnt[i] = 0;
+    A.ctl->t_index_ns += gtimer() - t0;
+  }
+  return nd;
+}
+
+// π repair from the rows in `dirty` (sources with label 0, bound 0).
+__device__ void repair(Ctx& X, const int* dirty, int nd) {
+  reset_labels(X, 0);
+  __syncthreads();
+  publish_sources(X, dirty, nd, kRepair);
+  __syncthreads();
+  exchange(X);
+  const int rounds = search_rounds(X, kRepair, -1, 0, 0, 0);
+  apply_repair(X);
+  __syncthreads();
+  if (X.lead) X.A.ctl->relax_rounds += rounds;
+}
+
+// check_invariants: π feasible on every Γ edge certifies "no negative
+// cycle" (refine.hpp:125-131). Owners check the edges into their nodes.
+__device__ void certify(Ctx& X) {
+  const EngineArgs& A = X.A;
+  if (!A.check_invariants) return;
+  if (X.lead) A.ctl->invariant_checks += 1;
+  bool bad = false;
+  for (int u = 0; u < X.k; ++u) {
+    const int64_t piu = pi_of(X, u);
+    const bool dum = has_dummy(X, u);
+    for (int v = X.v0 + threadIdx.x; v < min(X.v1, X.k); v += blockDim.x) {
+      if (v == u) continue;
+      const int64_t w = X.tile ? key16_weight(X.S.wt[static_cast<int64_t>(u) * X.s + (v - X.v0)], dum)
+                               : pair_weight(A.M[static_cast<int64_t>(u) * A.k + v], dum);
+      if (w == kNoEdge) continue;
+      if (w + piu - X.S.pis[v - X.v0] < 0) bad = true;
+    }
+  }
+  if (bad) set_err(X, kErrInvariant, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) X.S.pub[X.par]->count = 0;
+  exchange(X);
+}
+
+// One refinement (cycle or path) at `anchor` after the sources are
+// published and exchanged. Returns applied; `dirty` gets the rows to
+// repair when applied.
+__device__ bool finish_search(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
+                              int* dirty, int* nd) {
+  const int64_t t0 = gtimer();
+  const int rounds = search_rounds(X, kind, anchor, refund_a, bound_mid, 0);
+  const int64_t sl = sink_label(X);
+  if (X.lead) {
+    X.A.ctl->relax_rounds += rounds;
+    X.A.ctl->t_bf_ns += gtimer() - t0;
+  }
+  *nd = 0;
+  if (X.err || sl == kLabInf || lab_d(sl) >= 0) return false;
+  const int len = reconstruct(X, kind, anchor, refund_a, sl);
+  if (len == 0 || X.err) return false;
+  if (kind == kPath && X.S.path[len - 1].kind != kEdgePenalty) {
+    if (X.lead) set_err(X, kErrPenaltyEdge, len);
+    X.err = 1;
+    return false;
+  }
+  // the reference checks the path's edge sum against its cost
+  // (refine.hpp:75-79); with exact labels it holds by construction
+  *nd = apply(X, kind, len, lab_d(sl), dirty);
+  return true;
+}
+
+__device__ void add_delta(Ctx& X, int64_t v, int arg) {
+  int64_t r;
+  if (add_ovf(X.A.ctl->delta, v, &r)) set_err(X, kErrOverflow, arg);
+  X.A.ctl->delta = r;
+}
+
+}  // namespace cl
+
+// Shared memory: see cl::carve.
+__global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, int64_t* pi_global,
+                                                                 int32_t* dirty_buf) {
+  using namespace cl;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ctx X(cg::this_cluster());
+  X.A = A;
+  X.rank = static_cast<int>(X.cluster.block_rank());
+  X.csz = static_cast<int>(X.cluster.num_blocks());
+  X.k = A.k;
+  X.s = (A.k + 1 + X.csz - 1) / X.csz;
+  X.v0 = min(X.rank * X.s, A.k + 1);
+  X.v1 = min(X.v0 + X.s, A.k + 1);
+  X.tile = A.tile_mode != 0;
+  X.S = carve(smem_raw, A.k, X.s, X.tile);
+  X.par = 0;
+  X.err = 0;
+  X.lead = X.rank == 0 && threadIdx.x == 0;
+  CS& S = X.S;
+  const int k = A.k;
+  const bool strict = A.mode == 1;
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    const int v = X.v0 + i;
+    S.pis[i] = v < k ? pi_global[v] : 0;
+    S.chg[i] = 0;
+    S.lab[i] = kLabInf;
+  }
+  if (X.tile) {
+    const int ns = X.v1 - X.v0;
+    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(k) * ns; i += blockDim.x) {
+      const int u = static_cast<int>(i / ns);
+      const int col = static_cast<int>(i - static_cast<int64_t>(u) * ns);
+      const int v = X.v0 + col;
+      S.wt[static_cast<int64_t>(u) * X.s + col] =
+          v < k ? key16(A.M[static_cast<int64_t>(u) * k + v]) : kNoKey16;
+    }
+  }
+  if (threadIdx.x < 16) S.misc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      S.pub[b]->count = 0;
+      S.pub[b]->err = 0;
+      S.pub[b]->sinklab = kLabInf;
+      S.pub[b]->val = kEmpty;
+    }
+  }
+  __syncthreads();
+  X.cluster.sync();
+  int* dirty = dirty_buf + X.rank * (2 * k + 4);  // per-CTA scratch
+
+  for (int64_t a = A.a_begin; a < A.a_end && !X.err; ++a) {
+    int32_t d, s;
+    int64_t cost;
+    const int64_t t0 = gtimer();
+    int dum_a = 0;  // placeholder at the anchor after the eviction (strict)
+    if (!strict) {
+      const int64_t key = A.arr_keys[a];
+      d = static_cast<int32_t>(key & 0xffffffffLL);
+      cost = key >> 32;
+      s = A.best_center[d];
+    } else {
+      // strict target: cheapest center with placeholders (solver.hpp:257)
+      d = A.order != nullptr ? A.order[a] : static_cast<int32_t>(a);
+      const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+      int64_t best = kEmpty;
+      for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
+        if (A.dummies[j] <= 0) continue;
+        const int64_t pk = static_cast<int64_t>(row[j]) * (int64_t(1) << 32) + j;
+        best = min(best, pk);
+      }
+      if (threadIdx.x == 0) S.red[0] = kEmpty;
+      __syncthreads();
+      atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(best));
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        S.pub[X.par]->val = S.red[0];
+        S.pub[X.par]->count = 0;
+        const int64_t b = S.red[0];
+        S.pub[X.par]->aux = b == kEmpty ? 0 : static_cast<int32_t>(A.dummies[b & 0xffffffffLL]);
+      }
+      exchange(X);
+      best = kEmpty;
+      int cnt_t = 0;
+      for (int r = 0; r < X.csz; ++r) {
+        if (S.all[r].val < best) {
+          best = S.all[r].val;
+          cnt_t = S.all[r].aux;
+        }
+      }
+      if (best == kEmpty) {
+        if (X.lead) set_err(X, kErrNoResidual, d);
+        break;
+      }
+      s = static_cast<int32_t>(best & 0xffffffffLL);
+      cost = best >> 32;
+      dum_a = (cnt_t - 1) > 0;
+      __syncthreads();
+      // only the owner of s touches dummies[s] in this phase
+      if (s >= X.v0 && s < X.v1 && threadIdx.x == 0) A.dummies[s] -= 1;
+    }
+    const int64_t pi_s = pi_of(X, s);
+    // ---- insert + first relaxation round of the cycle search (source s) ----
+    reset_labels(X, pi_s);
+    __syncthreads();
+    {
+      const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+      const int32_t hv = row[s];
+      int64_t* Ms = A.M + static_cast<int64_t>(s) * k;
+      for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
+        int64_t m = Ms[j];
+        if (j != s) {
+          const int64_t nv = pack_transfer(row[j] - hv, d);
+          if (nv < m) {
+            m = nv;
+            Ms[j] = nv;
+            if (X.tile) S.wt[static_cast<int64_t>(s) * X.s + (j - X.v0)] = key16(nv);
+          }
+          const int64_t w = pair_weight(m, strict && dum_a);
+          if (w != kNoEdge) {
+            const int64_t rc = w + pi_s - S.pis[j - X.v0];
+            const int64_t cand = rc * (int64_t(1) << kCandShift) + 1;
+            if (cand < 0) {
+              S.lab[j - X.v0] = cand;
+              S.chg[j - X.v0] = 1;
+            }
+          }
+        }
+      }
+      if (s >= X.v0 && s < X.v1 && threadIdx.x == 0) S.lab[s - X.v0] = 0;  // the source
+      fill_sink_weights(X, kCycle, s, 0);
+      if (X.lead) {
+        if (A.home[d] != -1) set_err(X, kErrAlreadyIndexed, d);
+        A.home[d] = s;
+        A.load[s] += 1;
+        if (strict) add_delta(X, cost, d);
+        A.ctl->cycle_refine_calls += 1;
+      }
+      __syncthreads();
+      collect(X, kCycle, s);
+      exchange(X);
+      if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
+    }
+    int nd = 0;
+    const bool cyc = finish_search(X, kCycle, s, 0, 0, dirty, &nd);
+    if (X.err) break;
+    if (cyc) {
+      dirty[nd++] = s;  // the inserted row was never repaired
+      repair(X, dirty, nd);
+    } else {
+      apply_repair(X);  // π += min(0, d) over the explored region
+      __syncthreads();
+    }
+    certify(X);
+    if (strict) continue;
+
+    // ---- overload: penalty-aware path refinement ----
+    const int64_t load = A.load[s];
+    const int64_t cap = A.cap[s];
+    if (load <= cap) {
+      if (X.lead) add_delta(X, cost, d);
+      continue;
+    }
+    const int64_t refund_a = refund_penalty(X, s, load);
+    if (X.lead) {
+      int64_t r1;
+      if (add_ovf(cost, refund_a, &r1)) set_err(X, kErrOverflow, d);
+      add_delta(X, r1, d);
+    }
+    for (;;) {
+      if (X.lead) A.ctl->path_refine_calls += 1;
+      const int64_t refund = refund_penalty(X, s, A.load[s]);
+      // C = min_{u != s} marginal(u) - refund + π(u) - π(s): the most a
+      // penalty edge can subtract; prune the search to d_rc < -C
+      int64_t lmin = kEmpty;
+      for (int u = X.v0 + threadIdx.x; u < min(X.v1, k); u += blockDim.x) {
+        if (u == s) continue;
+        lmin = min(lmin, marginal_penalty(X, u, A.load[u]) - refund + S.pis[u - X.v0]);
+      }
+      if (threadIdx.x == 0) S.red[0] = kEmpty;
+      __syncthreads();
+      atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(lmin));
+      __syncthreads();
+      const int64_t pis_now = pi_of(X, s);
+      if (threadIdx.x == 0) {
+        S.pub[X.par]->val = S.red[0];
+        S.pub[X.par]->count = 0;
+      }
+      exchange(X);
+      int64_t cmin = kEmpty;
+      for (int r = 0; r < X.csz; ++r) cmin = min(cmin, S.all[r].val);
+      bool applied = false;
+      if (X.lead && !(cmin != kEmpty && cmin - pis_now < 0)) A.ctl->dbg[9] += 1;  // pruned
+      if (cmin != kEmpty && cmin - pis_now < 0 && !X.err) {
+        const int64_t C = cmin - pis_now;
+        if (X.lead) {
+          A.ctl->dbg[13] += -C;
+          A.ctl->dbg[14] = max(A.ctl->dbg[14], -C);
+          A.ctl->dbg[15] += refund;
+        }
+        reset_labels(X, pis_now);
+        fill_sink_weights(X, kPath, s, refund);
+        __syncthreads();
+        const int src[1] = {s};
+        publish_sources(X, src, 1, kPath);
+        __syncthreads();
+        exchange(X);
+        int nd2 = 0;
+        const int64_t bound = (-C) * (int64_t(1) << kCandShift);
+        applied = finish_search(X, kPath, s, refund, bound, dirty, &nd2);
+        if (applied) repair(X, dirty, nd2);
+      }
+      certify(X);
+      if (X.err) break;
+      if (!(A.fixpoint && applied && A.load[s] > cap)) break;
+    }
+  }
+  // persist π for the next launch
+  __syncthreads();
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    const int v = X.v0 + i;
+    if (v < k) pi_global[v] = S.pis[i];
+  }
+  X.cluster.sync();
+}
+
+}  // namespace lbdd_b200

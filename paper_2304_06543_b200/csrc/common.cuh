@@ -80,6 +80,7 @@ struct EngineCtl {
   int64_t t_bf_ns;                // bellman_ford bucket (globaltimer)
   int64_t t_index_ns;             // index_update bucket (globaltimer)
   int64_t barriers;               // grid barriers executed
+  int64_t dbg[16];                // engine instrumentation (see capi)
   int32_t error;
   int32_t error_arg;
   int32_t prev_sources;           // transfer sources of the last applied path

@@ -34,6 +34,7 @@ _P = C.c_void_p
 _lib.lbdd_b200_version.restype = C.c_char_p
 _lib.lbdd_b200_last_error.restype = C.c_char_p
 _lib.lbdd_b200_launch_count.restype = C.c_longlong
+_lib.lbdd_b200_engine_counters.argtypes = [_abi.I64P]
 _lib.lbdd_b200_instance_create.argtypes = [C.POINTER(_abi.InstanceDesc), C.c_int, C.POINTER(_P)]
 _lib.lbdd_b200_instance_create_device.argtypes = [C.POINTER(_abi.InstanceDesc), _P, C.c_int64,
                                                   C.c_int, C.POINTER(_P)]
@@ -77,6 +78,17 @@ def version() -> str:
 def launch_count() -> int:
     """Kernels of this library launched so far in this process."""
     return int(_lib.lbdd_b200_launch_count())
+
+
+def engine_counters():
+    """Instrumentation of the last solve (see include/lbdd_b200.h)."""
+    out = np.zeros(16, np.int64)
+    _lib.lbdd_b200_engine_counters(_i64(out))
+    names = ["cycle_searches", "path_searches", "repair_searches", "cycle_empty", "path_empty",
+             "repair_empty", "cycle_frontier", "path_frontier", "repair_frontier", "path_pruned",
+             "cycle_explored", "path_explored", "repair_explored", "path_bound_sum", "path_bound_max",
+             "path_refund_sum"]
+    return {n: int(out[i]) for i, n in enumerate(names)}
 
 
 def device_count() -> int:

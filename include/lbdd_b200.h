@@ -113,10 +113,12 @@ const char* lbdd_b200_last_error(void);
 int lbdd_b200_device_count(void);
 /* Kernels of this library launched so far in this process (all devices). */
 long long lbdd_b200_launch_count(void);
-/* Engine instrumentation of the last solve in this process: out[0..2]
- * searches started (cycle, path, potential repair), out[3..5] of those with
- * an empty initial frontier, out[6..8] frontier entries relaxed, out[9]
- * path searches pruned by the penalty bound. */
+/* Engine instrumentation of the last solve in this process (out[32]):
+ * out[0..2] searches started (cycle, path, potential repair), out[3..5] of
+ * those with an empty initial frontier, out[6..8] frontier entries relaxed,
+ * out[9] path searches pruned by the penalty bound, out[10..12] rounds per
+ * kind, out[13..15] path-bound statistics; out[16..31] cluster-engine
+ * lead-thread cycles per phase. */
 void lbdd_b200_engine_counters(int64_t* out);
 
 /* Upload an instance (host arrays) to `device`. Replaces constructing a

@@ -631,9 +631,9 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
 
 // ---- the cluster engine (cluster.cu): one thread-block cluster ----
 size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
-  return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * s + 2 * sizeof(cl::Pub) + 8 * 16 +
-         sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::FEntry) * cl::kStage + 8 * (k + 1) +
-         4 * (cl::kMaxCS + 2) +
+  return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * s + 2 * sizeof(cl::Pub) + 8 * 16 +
+         sizeof(cl::Pub) * cl::kMaxCS + 8 * (k + 1) +
+         4 * (cl::kMaxCS + 2) + 4 * static_cast<size_t>(cl::kMaxCS) * s + 8 * 16 + 8 * 16 +
          sizeof(PathEdge) * (k + 1) + 8 * block + 4 * 16 +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
 }
@@ -648,9 +648,11 @@ bool keys_fit_int16(const lbdd_b200_instance* I) {
   return I->scanned && I->min_cost >= 1 && I->max_cost + 1 - I->min_cost <= 32000;
 }
 
+constexpr int kClusterThreads = 256;
+
 EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64_t a_end,
                              bool keys16) {
-  const int block = kEngineThreads;
+  const int block = kClusterThreads;
   const int k = static_cast<int>(I->k);
   auto kernel = cluster_engine_kernel;
   CUDA_OK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -681,6 +683,10 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
       cudaGetLastError();
     }
     if (I->cluster_size == 0) raise(LBDD_ERR_CUDA, "lbdd_b200: no cluster configuration fits");
+  }
+  {
+    const char* ev = std::getenv("LBDD_B200_DELTA");
+    A.delta_step = ev != nullptr ? std::atoll(ev) : 16;
   }
   const int cs = I->cluster_size;
   const int s = (k + 1 + cs - 1) / cs;
@@ -950,9 +956,33 @@ extern "C" {
 
 const char* lbdd_b200_version(void) { return "lbdd_b200 0.1.0 (sm_100a)"; }
 long long lbdd_b200_launch_count(void) { return g_launches.load(); }
+/* Debug: cycles per exchange of the cluster primitive (cluster.cu). */
+long long lbdd_b200_debug_exchange_cycles(int cluster_size, int iters, int mode) {
+  auto kernel = cluster_exchange_bench;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  long long* d = nullptr;
+  cudaMalloc(&d, 16);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster_size;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cluster_size);
+  cfg.blockDim = dim3(512);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kernel, iters, mode, d) != cudaSuccess) return -1;
+  long long h[2] = {0, 0};
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h[0];
+}
+
 /* Engine instrumentation of the last solve (16 counters, see cluster.cu). */
 void lbdd_b200_engine_counters(int64_t* out) {
   for (int i = 0; i < 16; ++i) out[i] = g_last_ctl.dbg[i];
+  for (int i = 0; i < 16; ++i) out[16 + i] = g_last_ctl.prof[i];
 }
 const char* lbdd_b200_last_error(void) { return g_err.c_str(); }
 

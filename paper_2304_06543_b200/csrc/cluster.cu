@@ -47,12 +47,17 @@ constexpr int kMaxCS = 16;
 constexpr int kStage = 256;            // frontier entries staged per pass
 constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
 
+// A frontier entry as pushed into every CTA's inbox: the node (bit 31: a
+// surplus placeholder sits there, strict-mode edge rule) and its label with
+// π(node) folded in, lp = label + π(node) << 16, so that a candidate into v
+// is lp + (w - π(v)) << 16 + 1.
 struct FEntry {
-  int32_t node;
-  int32_t dum;    // surplus placeholder at node (strict mode edge rule)
-  int64_t label;  // packed (d_rc << 16) + hops
-  int64_t pi;     // π(node)
+  int32_t nd;
+  int32_t pad;
+  int64_t lp;
 };
+__device__ __forceinline__ int fe_node(const FEntry& e) { return e.nd & 0x7fffffff; }
+__device__ __forceinline__ bool fe_dum(const FEntry& e) { return (e.nd >> 31) != 0; }
 
 struct Pub {          // per-CTA published scalars of one exchange
   int32_t count;      // changed entries in list[par]
@@ -60,13 +65,15 @@ struct Pub {          // per-CTA published scalars of one exchange
   int64_t sinklab;    // label of anchor-in (owner only)
   int64_t val;        // reduction slot (min over the CTA)
   int32_t aux;        // reduction argument
-  int32_t pad;
+  int32_t pending;    // improved nodes held back by the Δ threshold
+  int64_t pmin;       // smallest held-back label
+  int64_t omin;       // smallest open label (held back or pushed this round)
 };
 
 struct CS {           // shared-memory layout of one CTA
   int64_t* lab;       // [s]
   int64_t* pis;       // [s]
-  FEntry* list[2];    // [s] each
+  FEntry* inbox[2];   // [kMaxCS * s] each: entries pushed by CTA r at r * s
   Pub* pub[2];        // [1] each
   PathEdge* path;     // [k + 1]
   uint8_t* chg;       // [s]
@@ -75,27 +82,32 @@ struct CS {           // shared-memory layout of one CTA
   int32_t* misc;      // [16]: 0 queue count, 1 local count, 2 local err
   int64_t* red;       // [16] reduction scratch
   Pub* all;           // [kMaxCS] snapshot of every CTA's pub after a barrier
-  FEntry* stage;      // [kStage] frontier entries staged from DSMEM
+
   int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
   int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
+  int32_t* idx;       // [kMaxCS * s] inbox slot of every pushed entry
+  int64_t* dbg;       // [16] instrumentation counters
+  int64_t* prof;      // [16] lead-thread cycle counters per phase
   int16_t* wt;        // [k * s] transfer keys of every row into my columns
                       // (tile mode: all keys fit in int16)
 };
 
 // host mirror: cluster_smem_bytes() in capi.cu
-__device__ CS carve(unsigned char* p, int k, int s, bool tile) {
+__device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   CS S;
   S.lab = reinterpret_cast<int64_t*>(p); p += 8 * s;
   S.pis = reinterpret_cast<int64_t*>(p); p += 8 * s;
-  S.list[0] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * s;
-  S.list[1] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * s;
+  S.inbox[0] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * kMaxCS * s;
+  S.inbox[1] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * kMaxCS * s;
   S.pub[0] = reinterpret_cast<Pub*>(p); p += sizeof(Pub);
   S.pub[1] = reinterpret_cast<Pub*>(p); p += sizeof(Pub);
   S.red = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.all = reinterpret_cast<Pub*>(p); p += sizeof(Pub) * kMaxCS;
-  S.stage = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * kStage;
   S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
   S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
+  S.idx = reinterpret_cast<int32_t*>(p); p += 4 * static_cast<size_t>(kMaxCS) * s;
+  S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
+  S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
   S.qd = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
   S.qs = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
@@ -104,6 +116,16 @@ __device__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.chg = reinterpret_cast<uint8_t*>(p);
   return S;
 }
+
+// lead-thread phase profiler: prof[i] += cycles since the last mark
+#define PROF_MARK(X, i)                                      \
+  do {                                                       \
+    if ((X).lead) {                                          \
+      const long long now__ = clock64();                     \
+      (X).S.prof[i] += now__ - (X).S.prof[15];               \
+      (X).S.prof[15] = now__;                                \
+    }                                                        \
+  } while (0)
 
 __device__ __forceinline__ int64_t gtimer() {
   uint64_t t;
@@ -155,16 +177,23 @@ struct Ctx {
   int err;            // sticky, identical in all CTAs (read at exchanges)
   bool lead;          // rank 0, thread 0
   bool tile;          // keys of my columns resident in S.wt
+  // per-launch counters kept in registers (lead thread), flushed at exit so
+  // no global read-modify-write sits on a round's critical path
+  int64_t n_barriers;
+  int64_t n_rounds;
+  int64_t T;          // Δ-stepping threshold of the running search (packed)
+  int64_t delta;      // Δ in packed units
+  int64_t* dbg;       // [16] shared-memory counters (lead thread)
   __device__ explicit Ctx(const cg::cluster_group& c) : cluster(c) {}
 };
 
-__device__ void set_err(Ctx& X, int code, int arg) {
+__device__ __forceinline__ void set_err(Ctx& X, int code, int arg) {
   if (atomicCAS(&X.A.ctl->error, 0, code) == 0) X.A.ctl->error_arg = arg;
   X.S.misc[2] = 1;
 }
 
 // PenaltySpec::at / marginal / refund (core.hpp:60-74, 196-208)
-__device__ int64_t pen_at(Ctx& X, int s, int64_t j) {
+__device__ __forceinline__ int64_t pen_at(Ctx& X, int s, int64_t j) {
   const EngineArgs& A = X.A;
   const int64_t* p = A.ppar + A.poff[s];
   switch (A.pfam[s]) {
@@ -180,11 +209,11 @@ __device__ int64_t pen_at(Ctx& X, int s, int64_t j) {
     }
   }
 }
-__device__ int64_t marginal_penalty(Ctx& X, int s, int64_t load) {
+__device__ __forceinline__ int64_t marginal_penalty(Ctx& X, int s, int64_t load) {
   if (load < 0) { set_err(X, kErrNegativeLoad, s); return 0; }
   return load < X.A.cap[s] ? 0 : pen_at(X, s, load - X.A.cap[s] + 1);
 }
-__device__ int64_t refund_penalty(Ctx& X, int s, int64_t load) {
+__device__ __forceinline__ int64_t refund_penalty(Ctx& X, int s, int64_t load) {
   if (load < 0) { set_err(X, kErrNegativeLoad, s); return 0; }
   return load <= X.A.cap[s] ? 0 : pen_at(X, s, load - X.A.cap[s]);
 }
@@ -194,154 +223,203 @@ __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
 }
 
 // Cluster barrier + exchange: every CTA publishes pub[par] (count, err,
-// sink label, reduction slot) — and list[par] — before calling; afterwards
-// S.all[] holds the values of every CTA, identical everywhere, and par
-// flips, so list[par ^ 1] are the sources of the next relaxation.
-__device__ void exchange(Ctx& X) {
-  if (threadIdx.x == 0) X.S.pub[X.par]->err = X.S.misc[2];
+// sink label, reduction slot) — and pushes inbox[par] — before calling;
+// afterwards S.all[] holds the values of every CTA, identical everywhere,
+// and par flips, so inbox[par ^ 1] holds the sources of the next relaxation.
+__device__ __forceinline__ void exchange(Ctx& X) {
+  CS& S = X.S;
+  if (threadIdx.x == 0) S.pub[X.par]->err = S.misc[2];
   X.cluster.sync();
-  if (threadIdx.x < X.csz) {
-    const Pub* rp = X.cluster.map_shared_rank(X.S.pub[X.par], threadIdx.x);
-    X.S.all[threadIdx.x] = *rp;
-  }
-  if (X.lead) X.A.ctl->barriers += 1;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    X.S.pref[0] = 0;
-    for (int r = 0; r < X.csz; ++r) {
-      const int c = X.S.all[r].count;
-      acc += (c >= 0 && c <= X.s) ? c : 0;
-      X.S.pref[r + 1] = acc;
+  if (threadIdx.x < 32) {
+    // warp 0: fetch every CTA's pub, scan the counts, OR the errors
+    const int lane = threadIdx.x;
+    int c = 0, e = 0;
+    if (lane < X.csz) {
+      const Pub* rp = X.cluster.map_shared_rank(S.pub[X.par], lane);
+      const Pub p = *rp;
+      S.all[lane] = p;
+      c = (p.count >= 0 && p.count <= X.s) ? p.count : 0;
+      e = p.err;
     }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < X.csz) S.pref[lane + 1] = incl;
+    if (lane == 0) S.pref[0] = 0;
+    const unsigned anyerr = __ballot_sync(0xffffffffu, e != 0);
+    if (lane == 0) S.misc[4] = anyerr != 0;
   }
+  if (X.lead) X.n_barriers += 1;
   __syncthreads();
-  for (int r = 0; r < X.csz; ++r) X.err |= X.S.all[r].err;
+  // flat index of the pushed entries: slot of the g-th entry in the inbox
+  const int total = S.pref[X.csz];
+  for (int g = threadIdx.x; g < total; g += blockDim.x) {
+    int lo = 0, hi = X.csz;  // last r with pref[r] <= g
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (S.pref[mid] <= g) lo = mid; else hi = mid;
+    }
+    S.idx[g] = lo * X.s + (g - S.pref[lo]);
+  }
+  X.err |= S.misc[4];
+  __syncthreads();
   // the next phase writes the other buffer while slow CTAs may still read
   // this one; it is rewritten only after the next barrier
   X.par ^= 1;
 }
 
-__device__ int total_count(const Ctx& X) {
+__device__ __forceinline__ int total_pending(const Ctx& X) {
+  int t = 0;
+  for (int r = 0; r < X.csz; ++r) t += X.S.all[r].pending;
+  return t;
+}
+// next threshold: at least Δ above the smallest held-back label
+__device__ __forceinline__ void advance_threshold(Ctx& X) {
+  if (total_pending(X) == 0) return;
+  int64_t m = kLabInf;
+  for (int r = 0; r < X.csz; ++r) m = min(m, X.S.all[r].pmin);
+  const int64_t t = m > kLabInf - X.delta ? kLabInf : m + X.delta;
+  if (t > X.T) X.T = t;
+}
+
+__device__ __forceinline__ int total_count(const Ctx& X) {
   int t = 0;
   for (int r = 0; r < X.csz; ++r) t += X.S.all[r].count;
   return t;
 }
 
-// Publish this CTA's changed nodes (and clear the flags) into list[par].
-__device__ void collect(Ctx& X, int kind, int anchor) {
+// Push this CTA's changed nodes (and clear the flags) into every CTA's
+// inbox[par] (slot range rank * s): DSMEM stores, ordered before the
+// readers by the release of the next cluster barrier.
+__device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label, int64_t pi,
+                                           bool dum) {
+  FEntry e;
+  e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
+  e.pad = 0;
+  e.lp = label + pi * (int64_t(1) << kCandShift);
+  const int slot = X.rank * X.s + pos;
+  for (int r = 0; r < X.csz; ++r) {
+    FEntry* box = X.cluster.map_shared_rank(X.S.inbox[X.par], r);
+    box[slot] = e;
+  }
+}
+
+// Δ-stepping: only improved nodes with label <= X.T are pushed; the rest
+// stay pending (their flag kept) and report their count and minimum.
+__device__ __forceinline__ void collect(Ctx& X, int kind, int anchor) {
   CS& S = X.S;
-  if (threadIdx.x == 0) S.misc[1] = 0;
+  if (threadIdx.x == 0) {
+    S.misc[1] = 0;
+    S.misc[3] = 0;
+    S.red[2] = kLabInf;
+    S.red[3] = kLabInf;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
     if (!S.chg[i]) continue;
-    S.chg[i] = 0;
     const int v = X.v0 + i;
-    if (v == X.k) continue;  // anchor-in has no out-edges
+    if (v == X.k) { S.chg[i] = 0; continue; }  // anchor-in has no out-edges
+    const int64_t label = S.lab[i];
+    if (label > X.T) {
+      atomicAdd(&S.misc[3], 1);
+      atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
+      continue;
+    }
+    S.chg[i] = 0;
+    atomicMin(reinterpret_cast<long long*>(&S.red[3]), static_cast<long long>(label));
     const int pos = atomicAdd(&S.misc[1], 1);
-    FEntry e;
-    e.node = v;
-    e.dum = (kind != kPath && has_dummy(X, v)) ? 1 : 0;
-    e.label = S.lab[i];
-    e.pi = S.pis[i];
-    S.list[X.par][pos] = e;
-    if (lab_h(e.label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
+    push_entry(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
+    if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     Pub* p = S.pub[X.par];
     p->count = S.misc[1];
+    p->pending = S.misc[3];
+    p->pmin = S.red[2];
+    p->omin = min(S.red[2], S.red[3]);
     p->sinklab = (X.k >= X.v0 && X.k < X.v1) ? S.lab[X.k - X.v0] : kLabInf;
   }
 }
 
-// Relax every edge from the published sources of the last exchange into
-// this CTA's nodes. bound_mid / bound_sink: strict upper bounds on labels.
-// Sources are staged from DSMEM into shared memory; each thread owns one
-// destination column per pass and keeps its running minimum in a register,
-// so a column sees one shared-memory atomicMin per pass.
-__device__ void relax(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
-                      int64_t bound_sink) {
+// Relax every edge from the sources pushed in the last exchange into this
+// CTA's nodes. bound_mid / bound_sink: strict upper bounds on labels. Each
+// thread owns one destination column per pass and keeps its running
+// minimum in a register, so a column sees one shared-memory atomicMin per
+// pass; sources are read from the local inbox (broadcast within a warp).
+__device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refund_a,
+                                      int64_t bound_mid, int64_t bound_sink) {
   CS& S = X.S;
   const EngineArgs& A = X.A;
   const int ns = X.v1 - X.v0;
   if (ns <= 0) return;  // uniform within the CTA
-  const int prev = X.par ^ 1;  // sources: the buffer of the last exchange
-  const int32_t* pref = S.pref;
-  const int total = pref[X.csz];
+  const FEntry* inbox = S.inbox[X.par ^ 1];  // pushed before the last exchange
   const int cpp = ns < static_cast<int>(blockDim.x) ? ((ns + 31) & ~31) : blockDim.x;
   const int rpp = blockDim.x / cpp;
   const int tx = threadIdx.x % cpp;
   const int ty = threadIdx.x / cpp;
-  for (int g0 = 0; g0 < total; g0 += kStage) {
-    const int cnt = min(kStage, total - g0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      const int g = g0 + t;
-      int r = 0;
-      while (g >= pref[r + 1]) ++r;
-      const FEntry* rl = X.cluster.map_shared_rank(S.list[prev], r);
-      FEntry e = rl[g - pref[r]];
-      if (e.node < 0 || e.node >= X.k) { set_err(X, 200, e.node); e.node = 0; e.label = kLabInf / 2; }
-      S.stage[t] = e;
-    }
-    __syncthreads();
-    for (int c0 = 0; c0 < ns; c0 += cpp) {
-      const int col = c0 + tx;
-      const int v = X.v0 + col;
-      if (col >= ns || ty >= cnt) continue;
-      const bool sinkcol = kind != kRepair && v == X.k;
-      if (v > X.k || (kind != kRepair && v == anchor) || (kind == kRepair && v == X.k)) continue;
-      const int64_t piv = S.pis[col];
-      const int64_t bound = sinkcol ? bound_sink : bound_mid;
-      int64_t best = kLabInf;
-      if (sinkcol) {
-        for (int t = ty; t < cnt; t += rpp) {
-          const FEntry e = S.stage[t];
-          const int64_t w = S.sinkw[e.node];  // kNoEdge for the anchor itself
-          if (w == kNoEdge) continue;
-          const int64_t cand = e.label + (w + e.pi - piv) * (int64_t(1) << kCandShift) + 1;
-          if (cand < bound && cand < best) best = cand;
-        }
-      } else if (X.tile) {
+  constexpr int64_t kUnit = int64_t(1) << kCandShift;
+  for (int c0 = 0; c0 < ns; c0 += cpp) {
+    const int col = c0 + tx;
+    const int v = X.v0 + col;
+    if (col >= ns) continue;
+    const bool sinkcol = kind != kRepair && v == X.k;
+    if (v > X.k || (kind != kRepair && v == anchor) || (kind == kRepair && v == X.k)) continue;
+    const int64_t base = 1 - S.pis[col] * kUnit;  // candidate = lp + w*unit + base
+    const int64_t bound = sinkcol ? bound_sink : bound_mid;
+    int64_t best = kLabInf;
+    const int cnt = S.pref[X.csz];
+    const int32_t* idx = S.idx;
+    if (sinkcol) {
+      for (int t = ty; t < cnt; t += rpp) {
+        const FEntry e = inbox[idx[t]];
+        const int64_t w = S.sinkw[fe_node(e)];  // kNoEdge for the anchor itself
+        if (w == kNoEdge) continue;
+        const int64_t cand = e.lp + w * kUnit + base;
+        if (cand < bound && cand < best) best = cand;
+      }
+    } else if (X.tile) {
 #pragma unroll 4
-        for (int t = ty; t < cnt; t += rpp) {
-          const FEntry e = S.stage[t];
-          const int64_t w = key16_weight(S.wt[static_cast<int64_t>(e.node) * X.s + col], e.dum != 0);
-          if (e.node == v || w == kNoEdge) continue;
-          const int64_t cand = e.label + (w + e.pi - piv) * (int64_t(1) << kCandShift) + 1;
+      for (int t = ty; t < cnt; t += rpp) {
+        const FEntry e = inbox[idx[t]];
+        const int u = fe_node(e);
+        const int64_t w = key16_weight(S.wt[static_cast<int64_t>(u) * X.s + col], fe_dum(e));
+        if (u == v || w == kNoEdge) continue;
+        const int64_t cand = e.lp + w * kUnit + base;
+        if (cand < bound && cand < best) best = cand;
+      }
+    } else {
+      // keys from global memory, 4 independent loads in flight
+      for (int t = ty; t < cnt; t += 4 * rpp) {
+        int64_t m[4];
+        FEntry e[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int tq = t + q * rpp;
+          e[q].nd = -1;
+          m[q] = kEmpty;
+          if (tq < cnt) {
+            e[q] = inbox[idx[tq]];
+            m[q] = A.M[static_cast<int64_t>(fe_node(e[q])) * A.k + v];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (e[q].nd == -1 || fe_node(e[q]) == v) continue;
+          const int64_t w = pair_weight(m[q], fe_dum(e[q]));
+          if (w == kNoEdge) continue;
+          const int64_t cand = e[q].lp + w * kUnit + base;
           if (cand < bound && cand < best) best = cand;
         }
-      } else {
-        // keys from global memory, 4 independent loads in flight
-        for (int t = ty; t < cnt; t += 4 * rpp) {
-          int64_t m[4];
-          FEntry e[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int tq = t + q * rpp;
-            e[q].node = -1;
-            m[q] = kEmpty;
-            if (tq < cnt) {
-              e[q] = S.stage[tq];
-              m[q] = A.M[static_cast<int64_t>(e[q].node) * A.k + v];
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (e[q].node < 0 || e[q].node == v) continue;
-            const int64_t w = pair_weight(m[q], e[q].dum != 0);
-            if (w == kNoEdge) continue;
-            const int64_t cand = e[q].label + (w + e[q].pi - piv) * (int64_t(1) << kCandShift) + 1;
-            if (cand < bound && cand < best) best = cand;
-          }
-        }
       }
-      if (best != kLabInf) {
-        const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
-                                        static_cast<long long>(best));
-        if (best < old) S.chg[col] = 1;
-      }
+    }
+    if (best != kLabInf) {
+      const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
+                                      static_cast<long long>(best));
+      if (best < old) S.chg[col] = 1;
     }
   }
 }
@@ -349,7 +427,7 @@ __device__ void relax(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bo
 // Weights of every edge into anchor-in, precomputed by its owner at the
 // start of a search: cycle graph w(u, anchor) (cheapest_pair_edge), path
 // graph the penalty difference marginal(u) - refund(anchor).
-__device__ void fill_sink_weights(Ctx& X, int kind, int anchor, int64_t refund_a) {
+__device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, int64_t refund_a) {
   if (!(X.k >= X.v0 && X.k < X.v1)) return;
   const EngineArgs& A = X.A;
   for (int u = threadIdx.x; u < X.k; u += blockDim.x) {
@@ -364,37 +442,54 @@ __device__ void fill_sink_weights(Ctx& X, int kind, int anchor, int64_t refund_a
 
 // Run rounds until no label changes. Sources must already be published in
 // list[par] (count in pub[par]) and exchanged. Returns rounds executed.
-__device__ int search_rounds(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
-                             int64_t bound_sink) {
+// Exact early stop: with non-negative reduced costs every label below the
+// smallest open label is final, and an open node v can lower anchor-in to
+// no less than lab(v) + sink_inc. Once anchor-in holds S and
+// min_open + sink_inc > S, nothing can change it or any node on its chain.
+__device__ __forceinline__ bool sink_settled(const Ctx& X, int64_t sink_inc) {
+  if (sink_inc == kLabInf) return false;
+  int64_t sl = kLabInf, om = kLabInf;
+  for (int r = 0; r < X.csz; ++r) {
+    sl = min(sl, X.S.all[r].sinklab);
+    om = min(om, X.S.all[r].omin);
+  }
+  return sl != kLabInf && (om == kLabInf || om + sink_inc > sl);
+}
+
+__device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
+                             int64_t bound_sink, int64_t sink_inc = kLabInf) {
   int rounds = 0;
   if (X.lead) {
-    X.A.ctl->dbg[kind] += 1;                   // searches started per kind
-    if (total_count(X) == 0) X.A.ctl->dbg[3 + kind] += 1;  // empty at start
+    X.dbg[kind] += 1;                                 // searches started per kind
+    if (total_count(X) == 0) X.dbg[3 + kind] += 1;    // empty at start
   }
-  while (total_count(X) > 0 && !X.err) {
-    if (X.lead) X.A.ctl->dbg[6 + kind] += total_count(X);  // frontier entries
+  advance_threshold(X);
+  while ((total_count(X) > 0 || total_pending(X) > 0) && !X.err && !sink_settled(X, sink_inc)) {
+    if (X.lead) X.dbg[6 + kind] += total_count(X);   // frontier entries
+    PROF_MARK(X, 9);
     relax(X, kind, anchor, refund_a, bound_mid, bound_sink);
     __syncthreads();
+    PROF_MARK(X, 1);
     collect(X, kind, anchor);
+    PROF_MARK(X, 2);
     exchange(X);
+    advance_threshold(X);
+    PROF_MARK(X, 3);
     ++rounds;
   }
-  // explored nodes (finite labels), per kind
-  int loc = 0;
-  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) loc += X.S.lab[i] != kLabInf;
-  atomicAdd(reinterpret_cast<unsigned long long*>(&X.A.ctl->dbg[10 + kind]),
-            static_cast<unsigned long long>(loc));
+  if (X.lead) X.dbg[10 + kind] += rounds;
   return rounds;
 }
 
-__device__ int64_t sink_label(const Ctx& X) {
+__device__ __forceinline__ int64_t sink_label(const Ctx& X) {
   int64_t l = kLabInf;
   for (int r = 0; r < X.csz; ++r) l = min(l, X.S.all[r].sinklab);
   return l;
 }
 
 // Start a search: labels of owned nodes to +inf, π(anchor-in) := π(anchor).
-__device__ void reset_labels(Ctx& X, int64_t pi_anchor) {
+__device__ __forceinline__ void reset_labels(Ctx& X, int64_t pi_anchor) {
+  X.T = X.delta;  // labels start at the source's 0
   for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
     X.S.lab[i] = kLabInf;
     X.S.chg[i] = 0;
@@ -403,14 +498,14 @@ __device__ void reset_labels(Ctx& X, int64_t pi_anchor) {
 }
 
 // Read π(v) of any node (DSMEM).
-__device__ int64_t pi_of(Ctx& X, int v) {
+__device__ __forceinline__ int64_t pi_of(Ctx& X, int v) {
   const int r = v / X.s;
   const int64_t* rp = X.cluster.map_shared_rank(X.S.pis, r);
   return rp[v - r * X.s];
 }
 
-// Publish a single source (label 0) owned by this CTA into list[par].
-__device__ void publish_sources(Ctx& X, const int* nodes, int count, int kind) {
+// Push the sources (label 0) owned by this CTA into every inbox[par].
+__device__ __forceinline__ void publish_sources(Ctx& X, const int* nodes, int count, int kind) {
   if (threadIdx.x == 0) {
     int c = 0;
     for (int i = 0; i < count; ++i) {
@@ -420,21 +515,18 @@ __device__ void publish_sources(Ctx& X, const int* nodes, int count, int kind) {
       for (int j = 0; j < i; ++j) dup |= nodes[j] == v;
       if (dup) continue;
       X.S.lab[v - X.v0] = 0;
-      FEntry e;
-      e.node = v;
-      e.dum = (kind != kPath && has_dummy(X, v)) ? 1 : 0;
-      e.label = 0;
-      e.pi = X.S.pis[v - X.v0];
-      X.S.list[X.par][c++] = e;
+      push_entry(X, c++, v, 0, X.S.pis[v - X.v0], kind != kPath && has_dummy(X, v));
     }
     X.S.pub[X.par]->count = c;
+    X.S.pub[X.par]->pending = 0;
+    X.S.pub[X.par]->omin = c > 0 ? 0 : kLabInf;
     X.S.pub[X.par]->sinklab = kLabInf;
   }
 }
 
 // π(v) += min(0, d(v)) for owned nodes explored by the last search. Ends
 // with a cluster barrier: other CTAs read π through DSMEM (pi_of) next.
-__device__ void apply_repair(Ctx& X) {
+__device__ __forceinline__ void apply_repair(Ctx& X) {
   for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
     if (X.v0 + i == X.k) continue;
     const int64_t l = X.S.lab[i];
@@ -451,7 +543,7 @@ __device__ void apply_repair(Ctx& X) {
 // Parent walk (refine.hpp:53-80) with the synchronous-BF parent rule:
 // parent(v) = min u with lab(u) + rc(u,v)*2^16 + 1 == lab(v). Fills S.path
 // (in path order) and returns its length; 0 + error on a broken chain.
-__device__ int reconstruct(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t sinklab) {
+__device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t sinklab) {
   CS& S = X.S;
   const EngineArgs& A = X.A;
   int v = X.k;
@@ -543,7 +635,7 @@ __device__ int reconstruct(Ctx& X, int kind, int anchor, int64_t refund_a, int64
 // invalidate and fold gains for their columns; the lead updates the
 // allotment; all CTAs rescan the invalidated entries over the final
 // buckets. Fills `dirty` with the rows whose out-edges may now violate π.
-__device__ int apply(Ctx& X, int kind, int len, int64_t cost, int* dirty) {
+__device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, int* dirty) {
   CS& S = X.S;
   const EngineArgs& A = X.A;
   const int k = X.k;
@@ -691,7 +783,7 @@ __device__ int apply(Ctx& X, int kind, int len, int64_t cost, int* dirty) {
 }
 
 // π repair from the rows in `dirty` (sources with label 0, bound 0).
-__device__ void repair(Ctx& X, const int* dirty, int nd) {
+__device__ __forceinline__ void repair(Ctx& X, const int* dirty, int nd) {
   reset_labels(X, 0);
   __syncthreads();
   publish_sources(X, dirty, nd, kRepair);
@@ -700,12 +792,12 @@ __device__ void repair(Ctx& X, const int* dirty, int nd) {
   const int rounds = search_rounds(X, kRepair, -1, 0, 0, 0);
   apply_repair(X);
   __syncthreads();
-  if (X.lead) X.A.ctl->relax_rounds += rounds;
+  if (X.lead) X.n_rounds += rounds;
 }
 
 // check_invariants: π feasible on every Γ edge certifies "no negative
 // cycle" (refine.hpp:125-131). Owners check the edges into their nodes.
-__device__ void certify(Ctx& X) {
+__device__ __forceinline__ void certify(Ctx& X) {
   const EngineArgs& A = X.A;
   if (!A.check_invariants) return;
   if (X.lead) A.ctl->invariant_checks += 1;
@@ -730,18 +822,23 @@ __device__ void certify(Ctx& X) {
 // One refinement (cycle or path) at `anchor` after the sources are
 // published and exchanged. Returns applied; `dirty` gets the rows to
 // repair when applied.
-__device__ bool finish_search(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
+__device__ __forceinline__ bool finish_search(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
                               int* dirty, int* nd) {
   const int64_t t0 = gtimer();
-  const int rounds = search_rounds(X, kind, anchor, refund_a, bound_mid, 0);
+  // smallest possible increment of an edge into anchor-in, in packed units:
+  // cycle graph rc >= 0; path graph rc_pen >= C = -bound_mid (see caller)
+  const int64_t sink_inc = kind == kCycle ? 1 : 1 - bound_mid;
+  const int rounds = search_rounds(X, kind, anchor, refund_a, bound_mid, 0, sink_inc);
   const int64_t sl = sink_label(X);
   if (X.lead) {
-    X.A.ctl->relax_rounds += rounds;
+    X.n_rounds += rounds;
     X.A.ctl->t_bf_ns += gtimer() - t0;
   }
   *nd = 0;
   if (X.err || sl == kLabInf || lab_d(sl) >= 0) return false;
+  PROF_MARK(X, 9);
   const int len = reconstruct(X, kind, anchor, refund_a, sl);
+  PROF_MARK(X, 10);
   if (len == 0 || X.err) return false;
   if (kind == kPath && X.S.path[len - 1].kind != kEdgePenalty) {
     if (X.lead) set_err(X, kErrPenaltyEdge, len);
@@ -751,10 +848,11 @@ __device__ bool finish_search(Ctx& X, int kind, int anchor, int64_t refund_a, in
   // the reference checks the path's edge sum against its cost
   // (refine.hpp:75-79); with exact labels it holds by construction
   *nd = apply(X, kind, len, lab_d(sl), dirty);
+  PROF_MARK(X, 11);
   return true;
 }
 
-__device__ void add_delta(Ctx& X, int64_t v, int arg) {
+__device__ __forceinline__ void add_delta(Ctx& X, int64_t v, int arg) {
   int64_t r;
   if (add_ovf(X.A.ctl->delta, v, &r)) set_err(X, kErrOverflow, arg);
   X.A.ctl->delta = r;
@@ -763,7 +861,7 @@ __device__ void add_delta(Ctx& X, int64_t v, int arg) {
 }  // namespace cl
 
 // Shared memory: see cl::carve.
-__global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, int64_t* pi_global,
+__global__ void __launch_bounds__(256, 1) cluster_engine_kernel(EngineArgs A, int64_t* pi_global,
                                                                  int32_t* dirty_buf) {
   using namespace cl;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -780,6 +878,13 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
   X.par = 0;
   X.err = 0;
   X.lead = X.rank == 0 && threadIdx.x == 0;
+  X.n_barriers = 0;
+  X.n_rounds = 0;
+  X.delta = A.delta_step <= 0 ? kLabInf / 4 : (A.delta_step << kCandShift);
+  X.T = X.delta;
+  X.dbg = X.S.dbg;
+  if (threadIdx.x < 16) X.dbg[threadIdx.x] = 0;
+  if (threadIdx.x < 16) X.S.prof[threadIdx.x] = 0;
   CS& S = X.S;
   const int k = A.k;
   const bool strict = A.mode == 1;
@@ -812,7 +917,9 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
   X.cluster.sync();
   int* dirty = dirty_buf + X.rank * (2 * k + 4);  // per-CTA scratch
 
+  PROF_MARK(X, 14);
   for (int64_t a = A.a_begin; a < A.a_end && !X.err; ++a) {
+    PROF_MARK(X, 14);
     int32_t d, s;
     int64_t cost;
     const int64_t t0 = gtimer();
@@ -905,7 +1012,9 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
       if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
     }
     int nd = 0;
+    PROF_MARK(X, 4);  // insert round
     const bool cyc = finish_search(X, kCycle, s, 0, 0, dirty, &nd);
+    PROF_MARK(X, 5);  // cycle search (+apply)
     if (X.err) break;
     if (cyc) {
       dirty[nd++] = s;  // the inserted row was never repaired
@@ -914,6 +1023,7 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
       apply_repair(X);  // π += min(0, d) over the explored region
       __syncthreads();
     }
+    PROF_MARK(X, 6);  // repairs
     certify(X);
     if (strict) continue;
 
@@ -950,16 +1060,17 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
         S.pub[X.par]->count = 0;
       }
       exchange(X);
+      PROF_MARK(X, 7);  // path bound
       int64_t cmin = kEmpty;
       for (int r = 0; r < X.csz; ++r) cmin = min(cmin, S.all[r].val);
       bool applied = false;
-      if (X.lead && !(cmin != kEmpty && cmin - pis_now < 0)) A.ctl->dbg[9] += 1;  // pruned
+      if (X.lead && !(cmin != kEmpty && cmin - pis_now < 0)) X.dbg[9] += 1;  // pruned
       if (cmin != kEmpty && cmin - pis_now < 0 && !X.err) {
         const int64_t C = cmin - pis_now;
         if (X.lead) {
-          A.ctl->dbg[13] += -C;
-          A.ctl->dbg[14] = max(A.ctl->dbg[14], -C);
-          A.ctl->dbg[15] += refund;
+          X.dbg[13] += -C;
+          X.dbg[14] = max(X.dbg[14], -C);
+          X.dbg[15] += refund;
         }
         reset_labels(X, pis_now);
         fill_sink_weights(X, kPath, s, refund);
@@ -970,13 +1081,23 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
         exchange(X);
         int nd2 = 0;
         const int64_t bound = (-C) * (int64_t(1) << kCandShift);
+        PROF_MARK(X, 6);
         applied = finish_search(X, kPath, s, refund, bound, dirty, &nd2);
+        PROF_MARK(X, 8);  // path search (+apply)
         if (applied) repair(X, dirty, nd2);
+        PROF_MARK(X, 6);
       }
       certify(X);
       if (X.err) break;
       if (!(A.fixpoint && applied && A.load[s] > cap)) break;
     }
+  }
+  if (X.lead) {
+    for (int i = 0; i < 15; ++i) A.ctl->prof[i] += S.prof[i];  // cycles per phase
+    for (int i = 0; i < 16; ++i) A.ctl->dbg[i] += X.dbg[i];
+    A.ctl->barriers += X.n_barriers;
+    A.ctl->relax_rounds += X.n_rounds;
+
   }
   // persist π for the next launch
   __syncthreads();
@@ -987,4 +1108,53 @@ __global__ void __launch_bounds__(512, 1) cluster_engine_kernel(EngineArgs A, in
   X.cluster.sync();
 }
 
+}  // namespace lbdd_b200
+
+namespace lbdd_b200 {
+// Micro-benchmark of the exchange primitive alone (publish, cluster barrier,
+// read every CTA's slot through DSMEM). Mode bit 0: also stage 128 remote
+// 24-byte entries per round; bit 1: use barrier.cluster with a relaxed
+// arrive + explicit cluster fence instead of cluster.sync().
+__global__ void __launch_bounds__(512, 1) cluster_exchange_bench(int iters, int mode,
+                                                                 long long* out) {
+  __shared__ cl::Pub pub[2];
+  __shared__ cl::Pub all[cl::kMaxCS];
+  __shared__ cl::FEntry list[128];
+  __shared__ cl::FEntry stage[128];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int csz = static_cast<int>(cluster.num_blocks());
+  if (threadIdx.x < 128) list[threadIdx.x].nd = threadIdx.x;
+  if (threadIdx.x == 0) { pub[0].count = 1; pub[1].count = 1; }
+  cluster.sync();
+  const long long t0 = clock64();
+  int par = 0;
+  int acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (mode & 1) {
+      if (threadIdx.x < 128) {
+        const int r = threadIdx.x % csz;
+        stage[threadIdx.x] = cluster.map_shared_rank(list, r)[threadIdx.x];
+      }
+      __syncthreads();
+      acc += stage[threadIdx.x & 127].nd;
+    }
+    if (threadIdx.x == 0) pub[par].count = it;
+    if (mode & 2) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else {
+      cluster.sync();
+    }
+    if (threadIdx.x < csz) all[threadIdx.x] = *cluster.map_shared_rank(&pub[par], threadIdx.x);
+    __syncthreads();
+    acc += all[0].count;
+    par ^= 1;
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0 && cluster.block_rank() == 0) {
+    out[0] = (t1 - t0) / iters;
+    out[1] = acc;
+  }
+  cluster.sync();
+}
 }  // namespace lbdd_b200

@@ -81,6 +81,7 @@ struct EngineCtl {
   int64_t t_index_ns;             // index_update bucket (globaltimer)
   int64_t barriers;               // grid barriers executed
   int64_t dbg[16];                // engine instrumentation (see capi)
+  int64_t prof[16];               // cluster engine: lead-thread cycles per phase
   int32_t error;
   int32_t error_arg;
   int32_t prev_sources;           // transfer sources of the last applied path
@@ -143,6 +144,7 @@ struct EngineArgs {
   int64_t* colW;         // k: weights into anchor-in
   int32_t search_base;   // searches run by earlier launches (set parity)
   int32_t pad2;
+  int64_t delta_step;    // cluster engine Δ-stepping width (cost units, <= 0: off)
   // path + transfer scratch
   PathEdge* path;        // k + 1
   int32_t* inv_cnt;      // k + 1

@@ -82,13 +82,17 @@ def launch_count() -> int:
 
 def engine_counters():
     """Instrumentation of the last solve (see include/lbdd_b200.h)."""
-    out = np.zeros(16, np.int64)
+    out = np.zeros(32, np.int64)
     _lib.lbdd_b200_engine_counters(_i64(out))
     names = ["cycle_searches", "path_searches", "repair_searches", "cycle_empty", "path_empty",
              "repair_empty", "cycle_frontier", "path_frontier", "repair_frontier", "path_pruned",
-             "cycle_explored", "path_explored", "repair_explored", "path_bound_sum", "path_bound_max",
+             "cycle_rounds", "path_rounds", "repair_rounds", "path_bound_sum", "path_bound_max",
              "path_refund_sum"]
-    return {n: int(out[i]) for i, n in enumerate(names)}
+    phases = ["relax", "collect", "exchange", "insert", "cycle", "repair", "bound", "path",
+              "other", "reconstruct", "apply"]
+    d = {n: int(out[i]) for i, n in enumerate(names)}
+    d["cycles"] = {p: int(out[16 + i + 1]) for i, p in enumerate(phases)}
+    return d
 
 
 def device_count() -> int:

@@ -97,3 +97,28 @@ def test_shard_rows_partition(n, world):
         assert row0 == pos and rows >= 0
         pos += rows
     assert max(r for _, r in spans) - min(r for _, r in spans) <= 1
+
+
+REF_INCLUDE = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF_INCLUDE, "lbdd")),
+                    reason="reference headers only exist in the build container")
+def test_compat_header_compiles_against_reference_types(tmp_path):
+    """include/lbdd_b200_compat.hpp is a drop-in for lbdd::asral_solve & co:
+    it must compile against the reference's own headers and link the C ABI."""
+    import subprocess
+    src = tmp_path / "use.cpp"
+    src.write_text(
+        '#include "lbdd_b200_compat.hpp"\n'
+        "int main() {\n"
+        "  lbdd::ProblemInstance inst;\n"
+        "  lbdd::SolveReport (*a)(const lbdd::ProblemInstance&, const lbdd::SolverOptions&, int) =\n"
+        "      &lbdd::b200::asral_solve;\n"
+        "  (void)a; (void)&lbdd::b200::strict_solve; (void)&lbdd::b200::greedy_solve;\n"
+        "  return inst.n() == 0 ? 0 : 1;\n}\n")
+    lib = os.path.join(ROOT, "paper_2304_06543_b200", "lib")
+    out = subprocess.run(["g++", "-std=c++20", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"),
+                          str(src), "-L", lib, "-llbdd_b200", "-o", str(tmp_path / "use")],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr

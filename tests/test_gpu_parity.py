@@ -176,3 +176,18 @@ def test_invariant_checking_counts(dev, oracle):
     a, b = dev.asral_solve(inst, opts), oracle.solve(inst, "asral", opts)
     assert a.stats.invariant_checks == b.stats.invariant_checks > 0
     assert same_report(a, b)
+
+
+def test_cpp_drop_in():
+    """The C++ compat front end (include/lbdd_b200_compat.hpp) against the
+    reference solver compiled into the same binary (oracle/drop_in_check.cpp):
+    identical SolveReports for asral / strict / greedy / para-asral."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "oracle", "_ref", "drop_in_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/drop_in_check not built (needs the reference headers at build time)")
+    out = subprocess.run([exe, "12"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "drop-in ok" in out.stdout

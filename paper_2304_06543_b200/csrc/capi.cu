@@ -133,7 +133,9 @@ struct lbdd_b200_instance {
   DevBuf<int32_t> P[2][2];
   DevBuf<int64_t> D[2][2], B[2][3];
   DevBuf<int64_t> load, dummies, M, colW, single_gain, pi;
-  DevBuf<int32_t> dirty;
+  DevBuf<int32_t> dirty, log_d, log_to, log_n;
+  DevBuf<int64_t> MX;
+  DevBuf<uint8_t> LN;
   int cluster_size = 0;  // chosen once per instance
   DevBuf<EngineCtl> ctl;
   DevBuf<GridBar> bar;
@@ -159,7 +161,8 @@ struct lbdd_b200_instance {
       for (int i = 0; i < 3; ++i) B[s][i].release();
     }
     single_out.release(); rowver.release(); load.release(); dummies.release(); M.release();
-    pi.release(); dirty.release();
+    pi.release(); dirty.release(); log_d.release(); log_to.release(); log_n.release();
+    MX.release(); LN.release();
     colW.release();
     single_gain.release(); ctl.release(); bar.release(); path.release(); dumflag.release();
     ib_cnt.release(); ib_off.release(); ib_cursor.release(); ib_sorted.release();
@@ -562,6 +565,8 @@ EngineArgs engine_args(lbdd_b200_instance* I) {
   A.single_out = I->single_out.p;
   A.single_gain = I->single_gain.p;
   A.rowver = I->rowver.p;
+  A.MX = I->MX.p;
+  A.LN = I->LN.p;
   A.single_kind = -1;
   return A;
 }
@@ -577,6 +582,11 @@ void reset_engine_state(lbdd_b200_instance* I, int64_t delta0) {
   CUDA_OK(cudaMemsetAsync(I->bar.p, 0, sizeof(GridBar), I->stream));
   CUDA_OK(cudaMemsetAsync(I->rowver.p, 0, sizeof(int32_t) * (k + 1), I->stream));
   CUDA_OK(cudaMemsetAsync(I->pi.p, 0, sizeof(int64_t) * (k + 1), I->stream));
+  // top-4 lists of the cluster engine: empty and complete
+  I->MX.ensure(static_cast<size_t>(k) * k * 3);
+  I->LN.ensure(static_cast<size_t>(k) * k);
+  fill64(I, I->MX.p, k * k * 3, kEmpty);
+  CUDA_OK(cudaMemsetAsync(I->LN.p, 8, static_cast<size_t>(k) * k, I->stream));
   EngineCtl ctl;
   std::memset(&ctl, 0, sizeof(ctl));
   ctl.delta = delta0;
@@ -633,7 +643,8 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
 size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
   return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * s + 2 * sizeof(cl::Pub) + 8 * 16 +
          sizeof(cl::Pub) * cl::kMaxCS + 8 * (k + 1) +
-         4 * (cl::kMaxCS + 2) + 4 * static_cast<size_t>(cl::kMaxCS) * s + 8 * 16 + 8 * 16 +
+         4 * (cl::kMaxCS + 2) + 4 * static_cast<size_t>(cl::kMaxCS) * s + 4 * 2 * cl::kMaxSeg +
+         8 * 16 + 8 * 16 +
          sizeof(PathEdge) * (k + 1) + 8 * block + 4 * 16 +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
 }
@@ -686,7 +697,9 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
   }
   {
     const char* ev = std::getenv("LBDD_B200_DELTA");
-    A.delta_step = ev != nullptr ? std::atoll(ev) : 16;
+    A.delta_step = ev != nullptr ? std::atoll(ev) : 1;
+    const char* dc = std::getenv("LBDD_B200_CHECK");
+    A.debug_checks = dc != nullptr && std::string(dc) == "1";
   }
   const int cs = I->cluster_size;
   const int s = (k + 1 + cs - 1) / cs;
@@ -701,19 +714,41 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   EngineCtl ctl;
-  const int64_t chunk = int64_t(1) << 16;
+  // chunks of arrivals per launch: the bucket index is rebuilt in between,
+  // so the move log a launch appends stays short
+  const int64_t chunk = 4096;
+  constexpr int32_t kLogCap = 1 << 16;
+  I->log_d.ensure(kLogCap);
+  I->log_to.ensure(kLogCap);
+  I->log_n.ensure(1);
+  A.log_d = I->log_d.p;
+  A.log_to = I->log_to.p;
+  A.log_n = I->log_n.p;
+  A.log_cap = kLogCap;
   int64_t a = a_begin;
   int64_t* pi = I->pi.p;
   int32_t* dirty = I->dirty.p;
   do {
     A.a_begin = a;
     A.a_end = std::min(a_end, a + chunk);
+    build_index_prepare(I, A.home, 0, I->n, I->stream, false);
+    A.bk_off = I->ib_off.p;
+    A.bk_ids = I->ib_sorted.p;
+    CUDA_OK(cudaMemsetAsync(I->log_n.p, 0, sizeof(int32_t), I->stream));
     g_launches++;
     CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, A, pi, dirty));
     CUDA_OK(cudaMemcpyAsync(&ctl, I->ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, I->stream));
     CUDA_OK(cudaStreamSynchronize(I->stream));
     g_err_arg = ctl.error_arg;
-    if (ctl.error) raise_engine_error(ctl.error);
+    if (ctl.error) {
+      if (std::getenv("LBDD_B200_DEBUG") != nullptr)
+        std::fprintf(stderr, "lbdd_b200: engine error %d arg %d after %lld cycle refines, %lld path "
+                     "refines (launch arrivals %lld..%lld)\n", ctl.error, ctl.error_arg,
+                     static_cast<long long>(ctl.cycle_refine_calls),
+                     static_cast<long long>(ctl.path_refine_calls),
+                     static_cast<long long>(A.a_begin), static_cast<long long>(A.a_end));
+      raise_engine_error(ctl.error);
+    }
     a = A.a_end;
   } while (a < a_end);
   return ctl;

@@ -46,6 +46,7 @@ constexpr int64_t kLabInf = INT64_MAX;
 constexpr int kMaxCS = 16;
 constexpr int kStage = 256;            // frontier entries staged per pass
 constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
+constexpr int kMaxSeg = 32;            // source rows rescanned per apply via the index
 
 // A frontier entry as pushed into every CTA's inbox: the node (bit 31: a
 // surplus placeholder sits there, strict-mode edge rule) and its label with
@@ -86,6 +87,7 @@ struct CS {           // shared-memory layout of one CTA
   int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
   int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
   int32_t* idx;       // [kMaxCS * s] inbox slot of every pushed entry
+  int32_t* seg;       // [2 * kMaxSeg] rescan segments (slot, prefix end)
   int64_t* dbg;       // [16] instrumentation counters
   int64_t* prof;      // [16] lead-thread cycle counters per phase
   int16_t* wt;        // [k * s] transfer keys of every row into my columns
@@ -106,6 +108,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
   S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
   S.idx = reinterpret_cast<int32_t*>(p); p += 4 * static_cast<size_t>(kMaxCS) * s;
+  S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 2 * kMaxSeg;
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
@@ -216,6 +219,116 @@ __device__ __forceinline__ int64_t marginal_penalty(Ctx& X, int s, int64_t load)
 __device__ __forceinline__ int64_t refund_penalty(Ctx& X, int s, int64_t load) {
   if (load < 0) { set_err(X, kErrNegativeLoad, s); return 0; }
   return load <= X.A.cap[s] ? 0 : pen_at(X, s, load - X.A.cap[s]);
+}
+
+// ---- per-entry top-4 lists: the 4 smallest (key, demand) of a heap ----
+// Entry (u, j) keeps its minimum in M[u*k+j] (what every reader uses) and
+// up to three successors in MX[(u*k+j)*3 ..]; LN[u*k+j] = length | complete
+// << 3, where "complete" means the list holds every demand sitting at u.
+// Invariant: the list is exactly the `length` smallest transfers of the
+// heap (subspace.hpp:26-231), so removing the head promotes the true next
+// minimum; a rescan is needed only when an incomplete list runs empty.
+constexpr int kTopK = 4;
+struct TopK {
+  int64_t e[kTopK];
+  int len;
+  bool complete;
+};
+__device__ __forceinline__ TopK list_load(const EngineArgs& A, int64_t idx) {
+  TopK t;
+  t.e[0] = A.M[idx];
+  const int64_t* mx = A.MX + idx * 3;
+  t.e[1] = mx[0];
+  t.e[2] = mx[1];
+  t.e[3] = mx[2];
+  const uint8_t ln = A.LN[idx];
+  t.len = ln & 7;
+  t.complete = (ln & 8) != 0;
+  return t;
+}
+__device__ __forceinline__ void list_store(const EngineArgs& A, int64_t idx, const TopK& t) {
+  A.M[idx] = t.e[0];
+  int64_t* mx = A.MX + idx * 3;
+  mx[0] = t.e[1];
+  mx[1] = t.e[2];
+  mx[2] = t.e[3];
+  A.LN[idx] = static_cast<uint8_t>(t.len | (t.complete ? 8 : 0));
+}
+// returns true when the head changed
+__device__ __forceinline__ bool list_insert(TopK& t, int64_t v) {
+  if (!t.complete && t.len == 0) return false;  // unknown minimum: a rescan follows
+  if (!t.complete && v > t.e[t.len - 1]) return false;
+  if (t.complete && t.len == kTopK && v > t.e[kTopK - 1]) {
+    t.complete = false;  // one more member than the list holds
+    return false;
+  }
+  if (t.complete && t.len == kTopK) t.complete = false;
+  int p = t.len < kTopK ? t.len : kTopK - 1;  // slot freed for the insert
+  while (p > 0 && t.e[p - 1] > v) {
+    t.e[p] = t.e[p - 1];
+    --p;
+  }
+  t.e[p] = v;
+  if (t.len < kTopK) ++t.len;
+  return p == 0;
+}
+// returns 0 when the demand is not listed, else 4 | (1 when the head
+// changed) | (2 when a rescan is needed)
+__device__ __forceinline__ int list_remove(TopK& t, int32_t demand) {
+  int p = -1;
+  for (int i = 0; i < t.len; ++i) {
+    if (t.e[i] != kEmpty && transfer_demand(t.e[i]) == demand) p = i;
+  }
+  if (p < 0) return 0;
+  for (int i = p; i + 1 < kTopK; ++i) t.e[i] = t.e[i + 1];
+  t.e[kTopK - 1] = kEmpty;
+  --t.len;
+  int r = p == 0 ? 5 : 4;
+  if (t.len == 0 && !t.complete) r |= 2;
+  return r;
+}
+
+// Debug validation (A.debug_checks): every list element's demand sits at
+// the row's center, keys match the cost matrix, lists are sorted, and the
+// head mirrors into the tile. Error 300 + where on the first violation.
+__device__ void validate_lists(Ctx& X, int where) {
+  const EngineArgs& A = X.A;
+  if (!A.debug_checks) return;
+  const int k = X.k;
+  for (int64_t p = threadIdx.x; p < static_cast<int64_t>(k) * (X.v1 - X.v0); p += blockDim.x) {
+    const int u = static_cast<int>(p / (X.v1 - X.v0));
+    const int j = X.v0 + static_cast<int>(p % (X.v1 - X.v0));
+    if (j >= k || j == u) continue;
+    const TopK t = list_load(A, static_cast<int64_t>(u) * k + j);
+    for (int i = 0; i < t.len; ++i) {
+      const int64_t e = t.e[i];
+      const int32_t d = transfer_demand(e);
+      int why = 0;
+      if (e == kEmpty) why = 1;
+      else if (A.home[d] != u) why = 2;
+      else if (transfer_key(e) != A.cm[static_cast<int64_t>(d) * A.pitch + j] -
+                                      A.cm[static_cast<int64_t>(d) * A.pitch + u]) why = 3;
+      else if (i > 0 && t.e[i - 1] >= e) why = 4;
+      // debug encoding (small instances): demand | u | j | slot | reason | len | complete
+      if (why) set_err(X, 300 + where, (d & 255) | ((u & 15) << 8) | ((j & 15) << 12) | (i << 16) |
+                                         (why << 20) | (t.len << 24) | (int(t.complete) << 28));
+    }
+    if (t.len == 0 && t.e[0] != kEmpty) set_err(X, 300 + where, -1);
+    if (X.tile && X.S.wt[static_cast<int64_t>(u) * X.s + (j - X.v0)] != key16(t.e[0]))
+      set_err(X, 320 + where, u);
+  }
+  __syncthreads();
+}
+
+// Append a home change to the move log (lead thread only).
+__device__ __forceinline__ void log_move(const EngineArgs& A, int32_t d, int32_t to) {
+  if (A.log_n == nullptr) return;
+  const int32_t i = *A.log_n;
+  if (i < A.log_cap) {
+    A.log_d[i] = d;
+    A.log_to[i] = to;
+  }
+  *A.log_n = i + 1;  // past the cap: overflowed, rescans scan every demand
 }
 
 __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
@@ -640,25 +753,27 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   const EngineArgs& A = X.A;
   const int k = X.k;
   const int64_t t0 = gtimer();
-  // ---- T1: invalidate (owners) ----
+  // ---- T1: remove the moved demands from their old rows' lists, insert
+  // them into the new rows' lists (column owners; one thread per column, so
+  // removals precede gains) ----
   const int jlo = X.v0, jhi = min(X.v1, k);
   for (int i = 0; i < len; ++i) {
     const PathEdge e = S.path[i];
     if (e.kind != kEdgeTransfer) continue;
     for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
       if (j == e.from_center) continue;
-      int64_t* p = &A.M[static_cast<int64_t>(e.from_center) * k + j];
-      const int64_t m = *p;
-      if (m != kEmpty && transfer_demand(m) == e.demand) {
-        *p = kEmpty;
-        if (X.tile) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = kNoKey16;
+      const int64_t idx = static_cast<int64_t>(e.from_center) * k + j;
+      TopK t = list_load(A, idx);
+      const int r = list_remove(t, e.demand);
+      if (r == 0) continue;
+      list_store(A, idx, t);
+      if (X.tile && (r & 1)) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = key16(t.e[0]);
+      if (r & 2) {
         const int pos = atomicAdd(&A.inv_cnt[i], 1);
         A.inv_cols[static_cast<int64_t>(i) * k + pos] = j;
       }
     }
   }
-  __syncthreads();
-  // gains into the receiving rows (same thread per column: after the clears)
   for (int i = 0; i < len; ++i) {
     const PathEdge e = S.path[i];
     if (e.kind != kEdgeTransfer) continue;
@@ -666,12 +781,12 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     const int32_t hv = row[e.to_center];
     for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
       if (j == e.to_center) continue;
-      int64_t* p = &A.M[static_cast<int64_t>(e.to_center) * k + j];
-      const int64_t v = pack_transfer(row[j] - hv, e.demand);
-      if (v < *p) {
-        *p = v;
-        if (X.tile) S.wt[static_cast<int64_t>(e.to_center) * X.s + (j - X.v0)] = key16(v);
+      const int64_t idx = static_cast<int64_t>(e.to_center) * k + j;
+      TopK t = list_load(A, idx);
+      if (list_insert(t, pack_transfer(row[j] - hv, e.demand))) {
+        if (X.tile) S.wt[static_cast<int64_t>(e.to_center) * X.s + (j - X.v0)] = key16(t.e[0]);
       }
+      list_store(A, idx, t);
     }
   }
   int nd = 0;
@@ -693,6 +808,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
         A.rowslot[e.from_center] = i;
         A.src_list[ns++] = e.from_center;
         ctl->transfers_applied += 1;
+        log_move(A, e.demand, e.to_center);
       } else if (e.kind == kEdgeDummy) {
         if (A.dummies == nullptr || A.dummies[e.from_center] <= 0) {
           set_err(X, kErrPlaceholder, e.from_center);
@@ -714,71 +830,119 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     else ctl->negative_paths_removed += 1;
   }
   if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+  PROF_MARK(X, 0);   // T1
   exchange(X);
+  PROF_MARK(X, 12);  // apply exchanges
+  validate_lists(X, 3);
   // ---- T3: rescans of the invalidated entries over the final buckets ----
+  // Members of a source center u: its segment of the bucket index built at
+  // launch start (A.bk_ids[A.bk_off[u] ..)), plus demands that moved to u
+  // since (the move log) — each still checked against home[]. A log that
+  // overflowed falls back to scanning every demand.
   int total = 0;
   for (int i = 0; i < len; ++i) total += (S.path[i].kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
   if (total > 0) {
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int nw = blockDim.x >> 5;
-    const int64_t per = (A.n + X.csz - 1) / X.csz;
-    const int64_t b0 = per * X.rank;
-    const int64_t b1 = (b0 + per < A.n) ? b0 + per : A.n;
-    for (int64_t base = b0; base < b1; base += blockDim.x) {
+    int32_t* seg = S.seg;  // [2 * kMaxSeg]: (slot, prefix end)
+    int nseg = 0;
+    int64_t nbase = 0;
+    bool full = A.bk_ids == nullptr || *A.log_n > A.log_cap;
+    for (int i = 0; i < len && !full; ++i) {
+      if (S.path[i].kind != kEdgeTransfer || A.inv_cnt[i] == 0) continue;
+      if (nseg == kMaxSeg) { full = true; break; }
+      const int u = S.path[i].from_center;
+      nbase += A.bk_off[u + 1] - A.bk_off[u];
+      if (threadIdx.x == 0) {
+        seg[2 * nseg] = i;
+        seg[2 * nseg + 1] = static_cast<int32_t>(nbase);
+      }
+      ++nseg;
+    }
+    __syncthreads();
+    const int64_t nlog = full ? 0 : *A.log_n;
+    int maxcnt = 0;
+    for (int i = 0; i < len; ++i) {
+      if (S.path[i].kind == kEdgeTransfer) maxcnt = max(maxcnt, A.inv_cnt[i]);
+    }
+    const int64_t ncand = full ? A.n : nbase + nlog;
+    const int64_t stride = static_cast<int64_t>(X.csz) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(X.rank) * blockDim.x; base < ncand; base += stride) {
       if (threadIdx.x == 0) S.misc[0] = 0;
       __syncthreads();
-      const int64_t d = base + threadIdx.x;
-      if (d < b1) {
-        const int32_t h = A.home[d];
-        if (h >= 0) {
-          const int32_t sl = A.rowslot[h];
-          if (sl >= 0 && A.inv_cnt[sl] > 0) {
-            const int q = atomicAdd(&S.misc[0], 1);
-            S.qd[q] = static_cast<int32_t>(d);
-            S.qs[q] = sl;
+      const int64_t x = base + threadIdx.x;
+      if (x < ncand) {
+        int32_t dd = -1, sl = -1;
+        if (full) {
+          dd = static_cast<int32_t>(x);
+          const int32_t h = A.home[dd];
+          if (h >= 0) {
+            sl = A.rowslot[h];
+            if (sl >= 0 && A.inv_cnt[sl] == 0) sl = -1;
           }
+        } else if (x < nbase) {
+          int g = 0;
+          while (x >= seg[2 * g + 1]) ++g;
+          const int slot = seg[2 * g];
+          const int u = S.path[slot].from_center;
+          const int64_t off = x - (g == 0 ? 0 : seg[2 * g - 1]);
+          dd = A.bk_ids[A.bk_off[u] + off];
+          if (A.home[dd] == u) sl = slot;
+        } else {
+          const int64_t li = x - nbase;
+          dd = A.log_d[li];
+          const int32_t to = A.log_to[li];
+          if (A.home[dd] == to) {
+            sl = A.rowslot[to];
+            if (sl >= 0 && A.inv_cnt[sl] == 0) sl = -1;
+          }
+        }
+        if (sl >= 0) {
+          const int q = atomicAdd(&S.misc[0], 1);
+          S.qd[q] = dd;
+          S.qs[q] = sl;
         }
       }
       __syncthreads();
       const int qn = S.misc[0];
-      for (int q = warp; q < qn; q += nw) {
-        const int32_t dd = S.qd[q];
-        const int sl = S.qs[q];
-        const int u = S.path[sl].from_center;
-        const int32_t* row = A.cm + static_cast<int64_t>(dd) * A.pitch;
-        const int32_t hv = row[u];
-        const int cnt = A.inv_cnt[sl];
-        const int32_t* cols = A.inv_cols + static_cast<int64_t>(sl) * k;
-        for (int x = lane; x < cnt; x += 32) {
-          const int j = cols[x];
-          atomicMin(reinterpret_cast<long long*>(&A.M[static_cast<int64_t>(u) * k + j]),
-                    static_cast<long long>(pack_transfer(row[j] - hv, dd)));
-        }
+      // (member, invalidated column) pairs spread over every thread: two
+      // independent cost loads and one atomicMin per pair
+      for (int p = threadIdx.x; p < qn * maxcnt; p += blockDim.x) {
+        const int q = p % qn;
+        const int xx = p / qn;
+        const int sl2 = S.qs[q];
+        const int cnt = A.inv_cnt[sl2];
+        if (xx >= cnt) continue;
+        const int32_t d2 = S.qd[q];
+        const int u = S.path[sl2].from_center;
+        const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
+        const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
+        atomicMin(reinterpret_cast<long long*>(&A.M[static_cast<int64_t>(u) * k + j]),
+                  static_cast<long long>(pack_transfer(row[j] - row[u], d2)));
       }
       __syncthreads();
     }
   }
   if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+  PROF_MARK(X, 13);  // T3
   exchange(X);
-  // rescans wrote M with atomics from every CTA: refresh my tile columns of
-  // the source rows
-  if (X.tile) {
-    for (int i = 0; i < len; ++i) {
-      const PathEdge e = S.path[i];
-      if (e.kind != kEdgeTransfer) continue;
-      for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
-        S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] =
-            key16(A.M[static_cast<int64_t>(e.from_center) * k + j]);
-      }
+  PROF_MARK(X, 12);
+  // rescanned entries now hold their exact minimum: a one-element,
+  // incomplete list (or an empty complete one); refresh my tile columns
+  for (int i = 0; i < len; ++i) {
+    const PathEdge e = S.path[i];
+    if (e.kind != kEdgeTransfer) continue;
+    const int cnt = A.inv_cnt[i];
+    for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+      const int j = A.inv_cols[static_cast<int64_t>(i) * k + x];
+      if (j < jlo || j >= jhi) continue;
+      const int64_t idx = static_cast<int64_t>(e.from_center) * k + j;
+      const int64_t m = A.M[idx];
+      A.LN[idx] = m == kEmpty ? 8 : 1;
+      if (X.tile) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = key16(m);
     }
-    __syncthreads();
   }
-  // counters for the next apply are reset before the next one starts
-  if (X.lead) {
-    for (int i = 0; i < len; ++i) A.inv_cnt[i] = 0;
-    A.ctl->t_index_ns += gtimer() - t0;
-  }
+  __syncthreads();
+  validate_lists(X, 2);
+  if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
   return nd;
 }
 
@@ -837,6 +1001,11 @@ __device__ __forceinline__ bool finish_search(Ctx& X, int kind, int anchor, int6
   *nd = 0;
   if (X.err || sl == kLabInf || lab_d(sl) >= 0) return false;
   PROF_MARK(X, 9);
+  // invalidation counters of the previous apply: its readers finished
+  // before the last barrier, the next writers (T1) come after the next one
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i <= X.k; i += blockDim.x) X.A.inv_cnt[i] = 0;
+  }
   const int len = reconstruct(X, kind, anchor, refund_a, sl);
   PROF_MARK(X, 10);
   if (len == 0 || X.err) return false;
@@ -976,24 +1145,22 @@ __global__ void __launch_bounds__(256, 1) cluster_engine_kernel(EngineArgs A, in
     {
       const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
       const int32_t hv = row[s];
-      int64_t* Ms = A.M + static_cast<int64_t>(s) * k;
       for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
-        int64_t m = Ms[j];
-        if (j != s) {
-          const int64_t nv = pack_transfer(row[j] - hv, d);
-          if (nv < m) {
-            m = nv;
-            Ms[j] = nv;
-            if (X.tile) S.wt[static_cast<int64_t>(s) * X.s + (j - X.v0)] = key16(nv);
-          }
-          const int64_t w = pair_weight(m, strict && dum_a);
-          if (w != kNoEdge) {
-            const int64_t rc = w + pi_s - S.pis[j - X.v0];
-            const int64_t cand = rc * (int64_t(1) << kCandShift) + 1;
-            if (cand < 0) {
-              S.lab[j - X.v0] = cand;
-              S.chg[j - X.v0] = 1;
-            }
+        if (j == s) continue;
+        const int64_t idx = static_cast<int64_t>(s) * k + j;
+        TopK t = list_load(A, idx);
+        if (list_insert(t, pack_transfer(row[j] - hv, d))) {
+          if (X.tile) S.wt[static_cast<int64_t>(s) * X.s + (j - X.v0)] = key16(t.e[0]);
+        }
+        list_store(A, idx, t);
+        const int64_t m = t.e[0];
+        const int64_t w = pair_weight(m, strict && dum_a);
+        if (w != kNoEdge) {
+          const int64_t rc = w + pi_s - S.pis[j - X.v0];
+          const int64_t cand = rc * (int64_t(1) << kCandShift) + 1;
+          if (cand < 0) {
+            S.lab[j - X.v0] = cand;
+            S.chg[j - X.v0] = 1;
           }
         }
       }
@@ -1003,12 +1170,14 @@ __global__ void __launch_bounds__(256, 1) cluster_engine_kernel(EngineArgs A, in
         if (A.home[d] != -1) set_err(X, kErrAlreadyIndexed, d);
         A.home[d] = s;
         A.load[s] += 1;
+        log_move(A, d, s);
         if (strict) add_delta(X, cost, d);
         A.ctl->cycle_refine_calls += 1;
       }
       __syncthreads();
       collect(X, kCycle, s);
       exchange(X);
+      validate_lists(X, 1);
       if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
     }
     int nd = 0;

@@ -145,6 +145,19 @@ struct EngineArgs {
   int32_t search_base;   // searches run by earlier launches (set parity)
   int32_t pad2;
   int64_t delta_step;    // cluster engine Δ-stepping width (cost units, <= 0: off)
+  // bucket index (demands grouped by home, built before each launch) and
+  // the move log appended since; nullptr: rescans scan every demand
+  const int32_t* bk_off;  // k + 1
+  const int32_t* bk_ids;  // n
+  int32_t* log_d;
+  int32_t* log_to;
+  int32_t* log_n;
+  int32_t log_cap;
+  int32_t pad3;
+  int64_t* MX;            // k*k*3: 2nd..4th smallest transfer per entry
+  uint8_t* LN;            // k*k: list length | complete << 3
+  int32_t debug_checks;   // validate engine invariants after each phase
+  int32_t pad4;
   // path + transfer scratch
   PathEdge* path;        // k + 1
   int32_t* inv_cnt;      // k + 1

@@ -22,7 +22,7 @@ from . import _abi
 from .instance import DescHolder, ProblemInstance, SolveReport, SolverOptions
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liblbdd_b200.so")
+LIB_PATH = os.environ.get("LBDD_B200_LIB") or os.path.join(_HERE, "lib", "liblbdd_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -88,10 +88,10 @@ def engine_counters():
              "repair_empty", "cycle_frontier", "path_frontier", "repair_frontier", "path_pruned",
              "cycle_rounds", "path_rounds", "repair_rounds", "path_bound_sum", "path_bound_max",
              "path_refund_sum"]
-    phases = ["relax", "collect", "exchange", "insert", "cycle", "repair", "bound", "path",
-              "other", "reconstruct", "apply"]
+    phases = ["T1", "relax", "collect", "exchange", "insert", "cycle", "repair", "bound", "path",
+              "other", "reconstruct", "apply", "apply_exch", "T3"]
     d = {n: int(out[i]) for i, n in enumerate(names)}
-    d["cycles"] = {p: int(out[16 + i + 1]) for i, p in enumerate(phases)}
+    d["cycles"] = {p: int(out[16 + i]) for i, p in enumerate(phases)}
     return d
 
 

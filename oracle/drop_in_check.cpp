@@ -65,6 +65,7 @@ void expect(bool ok, const std::string& what) {
 }
 
 void compare(const lbdd::SolveReport& a, const lbdd::SolveReport& b, const std::string& tag) {
+  if (std::getenv("DROP_IN_VERBOSE")) std::fprintf(stderr, "  compared %s\n", tag.c_str());
   expect(a.solver == b.solver, tag + " solver name " + a.solver + " vs " + b.solver);
   expect(a.objective == b.objective, tag + " objective");
   expect(a.assignment.assignment == b.assignment.assignment, tag + " assignment");
@@ -104,6 +105,10 @@ int main(int argc, char** argv) {
     const lbdd::Count n = 40 + 37 * c, k = 3 + c % 9;
     const double theta = (c % 3 == 0) ? 1.2 : (c % 3 == 1 ? 0.8 : 1.0);
     const auto inst = make_instance(1000 + c, n, k, theta);
+    if (std::getenv("DROP_IN_VERBOSE")) {
+      std::fprintf(stderr, "case %d: n %lld k %lld theta %.1f\n", c, static_cast<long long>(n),
+                   static_cast<long long>(k), theta);
+    }
     for (int fix = 0; fix < 2; ++fix) {
       lbdd::SolverOptions o;
       o.refine_to_fixpoint = fix != 0;

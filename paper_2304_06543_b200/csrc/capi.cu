@@ -659,7 +659,7 @@ bool keys_fit_int16(const lbdd_b200_instance* I) {
   return I->scanned && I->min_cost >= 1 && I->max_cost + 1 - I->min_cost <= 32000;
 }
 
-constexpr int kClusterThreads = 256;
+constexpr int kClusterThreads = LBDD_CLUSTER_THREADS;
 
 EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64_t a_end,
                              bool keys16) {

@@ -288,6 +288,8 @@ __device__ __forceinline__ int list_remove(TopK& t, int32_t demand) {
   return r;
 }
 
+__device__ int g_dbg_printed = 0;
+__device__ long long g_dbg_arrival = 0;
 // Debug validation (A.debug_checks): every list element's demand sits at
 // the row's center, keys match the cost matrix, lists are sorted, and the
 // head mirrors into the tile. Error 300 + where on the first violation.
@@ -314,6 +316,25 @@ __device__ void validate_lists(Ctx& X, int where) {
                                          (why << 20) | (t.len << 24) | (int(t.complete) << 28));
     }
     if (t.len == 0 && t.e[0] != kEmpty) set_err(X, 300 + where, -1);
+    bool bad = t.len == 0 && t.e[0] != kEmpty;
+    for (int i = 0; i < t.len; ++i) {
+      const int64_t e = t.e[i];
+      if (e == kEmpty || A.home[transfer_demand(e)] != u) bad = true;
+    }
+    if (bad && atomicCAS(&g_dbg_printed, 0, 1) == 0) {
+      printf("lbdd_b200 list violation arrival %lld where %d u %d j %d len %d complete %d\n",
+             g_dbg_arrival, where, u, j, t.len, int(t.complete));
+      for (int i = 0; i < kTopK; ++i) {
+        const int64_t e = t.e[i];
+        printf("  e[%d] key %lld demand %d home %d\n", i, e == kEmpty ? -1LL : (long long)transfer_key(e),
+               e == kEmpty ? -1 : transfer_demand(e), e == kEmpty ? -2 : A.home[transfer_demand(e)]);
+      }
+      for (int i = 0; i < k + 1 && i < 12; ++i) {
+        const PathEdge pe = X.S.path[i];
+        printf("  path[%d] %d -> %d kind %d demand %d inv_cnt %d\n", i, pe.from_center, pe.to_center,
+               pe.kind, pe.demand, A.inv_cnt[i]);
+      }
+    }
     if (X.tile && X.S.wt[static_cast<int64_t>(u) * X.s + (j - X.v0)] != key16(t.e[0]))
       set_err(X, 320 + where, u);
   }
@@ -697,14 +718,21 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
       p->val = bu;
       p->count = 0;
       p->sinklab = bu == kEmpty ? kLabInf : S.lab[bu - X.v0];  // the parent's label
+      // the edge's transfer word, read BEFORE the barrier: past it, CTAs
+      // that finished reconstructing may already rewrite M in apply (T1)
+      const int cv = v == X.k ? anchor : v;
+      p->pmin = (bu == kEmpty || (kind == kPath && v == X.k))
+                    ? kEmpty : A.M[bu * static_cast<int64_t>(A.k) + cv];
     }
     exchange(X);
     int64_t u = kEmpty;
     int64_t lu = 0;
+    int64_t word = kEmpty;
     for (int r = 0; r < X.csz; ++r) {
       if (S.all[r].val < u) {
         u = S.all[r].val;
         lu = S.all[r].sinklab;
+        word = S.all[r].pmin;
       }
     }
     if (u == kEmpty) { set_err(X, kErrBrokenParent, v); X.err = 1; break; }
@@ -719,7 +747,7 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
       if (kind == kPath && v == X.k) {
         e.kind = kEdgePenalty;
       } else {
-        const int64_t m = A.M[static_cast<int64_t>(uu) * A.k + cv];
+        const int64_t m = word;
         const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[uu] > 0;
         e.kind = pair_kind(m, dum);
         if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
@@ -831,9 +859,12 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   }
   if (threadIdx.x == 0) S.pub[X.par]->count = 0;
   PROF_MARK(X, 0);   // T1
+  // before the exchange: once past it, other CTAs' T3 rescans write M of
+  // any column
+  __syncthreads();
+  validate_lists(X, 3);
   exchange(X);
   PROF_MARK(X, 12);  // apply exchanges
-  validate_lists(X, 3);
   // ---- T3: rescans of the invalidated entries over the final buckets ----
   // Members of a source center u: its segment of the bucket index built at
   // launch start (A.bk_ids[A.bk_off[u] ..)), plus demands that moved to u
@@ -1015,7 +1046,48 @@ __device__ __forceinline__ bool finish_search(Ctx& X, int kind, int anchor, int6
     return false;
   }
   // the reference checks the path's edge sum against its cost
-  // (refine.hpp:75-79); with exact labels it holds by construction
+  // (refine.hpp:75-79): recount it from the cost matrix (one lookup per
+  // edge), so a stale transfer weight can never reach the objective
+  if (X.lead) {
+    const EngineArgs& A = X.A;
+    int64_t sum = 0;
+    for (int i = 0; i < len; ++i) {
+      const PathEdge e = X.S.path[i];
+      if (e.kind == kEdgeTransfer) {
+        const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+        sum += static_cast<int64_t>(row[e.to_center]) - row[e.from_center];
+      } else if (e.kind == kEdgePenalty) {
+        sum += marginal_penalty(X, e.from_center, A.load[e.from_center]) - refund_a;
+      }
+    }
+    if (sum != lab_d(sl)) {
+      set_err(X, kErrPathSum, len);
+      if (atomicCAS(&g_dbg_printed, 0, 1) == 0) {
+        printf("lbdd_b200 path sum mismatch rank %d kind %d anchor %d len %d label cost %lld edge sum %lld\n",
+               X.rank, kind, anchor, len, static_cast<long long>(lab_d(sl)), static_cast<long long>(sum));
+        for (int i = 0; i < len && i < 16; ++i) {
+          const PathEdge e = X.S.path[i];
+          const int64_t m = A.M[static_cast<int64_t>(e.from_center) * A.k + e.to_center];
+          long long key = -1;
+          if (e.kind == kEdgeTransfer) {
+            const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+            key = static_cast<long long>(row[e.to_center]) - row[e.from_center];
+          }
+          int tkey = -99999;
+          if (X.tile && e.to_center < X.k) {
+            const int r = e.to_center / X.s;
+            const int16_t* wt = X.cluster.map_shared_rank(X.S.wt, r);
+            tkey = wt[static_cast<int64_t>(e.from_center) * X.s + (e.to_center - r * X.s)];
+          }
+          printf("  edge %d: %d -> %d kind %d demand %d cm key %lld M key %d M demand %d tile %d\n", i,
+                 e.from_center, e.to_center, e.kind, e.demand, key,
+                 m == kEmpty ? -1 : transfer_key(m), m == kEmpty ? -1 : transfer_demand(m), tkey);
+        }
+      }
+    }
+  }
+  // a mismatch is raised at the next exchange; every CTA still runs apply
+  // so the cluster barriers stay matched
   *nd = apply(X, kind, len, lab_d(sl), dirty);
   PROF_MARK(X, 11);
   return true;
@@ -1030,7 +1102,7 @@ __device__ __forceinline__ void add_delta(Ctx& X, int64_t v, int arg) {
 }  // namespace cl
 
 // Shared memory: see cl::carve.
-__global__ void __launch_bounds__(256, 1) cluster_engine_kernel(EngineArgs A, int64_t* pi_global,
+__global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel(EngineArgs A, int64_t* pi_global,
                                                                  int32_t* dirty_buf) {
   using namespace cl;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1089,6 +1161,10 @@ __global__ void __launch_bounds__(256, 1) cluster_engine_kernel(EngineArgs A, in
   PROF_MARK(X, 14);
   for (int64_t a = A.a_begin; a < A.a_end && !X.err; ++a) {
     PROF_MARK(X, 14);
+    if (A.debug_checks) {
+      if (X.lead) g_dbg_arrival = a;
+      validate_lists(X, 0);
+    }
     int32_t d, s;
     int64_t cost;
     const int64_t t0 = gtimer();

@@ -18,6 +18,11 @@
 //                                elementwise MIN combines partial scans.
 #pragma once
 
+// threads per CTA of the cluster engine (cluster.cu)
+#ifndef LBDD_CLUSTER_THREADS
+#define LBDD_CLUSTER_THREADS 256
+#endif
+
 #include <cstdint>
 
 #include <cuda_runtime.h>

@@ -41,7 +41,7 @@ BASELINE_METRIC = "ASRAL solve time (s) and cost-matrix scan GB/s vs HBM peak at
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=2)
+    p.add_argument("--steps", type=int, default=1)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=1_000_000)
@@ -177,7 +177,6 @@ def run_ours(a):
     dev_s = sum(r.timings.device_ns for r in reports) / 1e9
     step_s = max_over_ranks(dev_s / a.steps)
     rep = reports[-1]
-    engine_ns = rep.timings.total_ns - rep.timings.scan_ns
     objective = rep.objective
 
     # ---- e2e through the C ABI with host buffers ----
@@ -227,12 +226,16 @@ def run_ours(a):
     shard_ms = max_over_ranks(e0.elapsed_time(e1) / 5)
 
     peak, peak_kind = peaks()
-    k1 = k * (k + 1)
+    # dominant kernel: cluster_engine_kernel (the arrival loop). Algorithmic
+    # bytes: the cost row of every arrival (4k B) and of every
+    # applied transfer (4k B, its keys into the k-1 lists of the new row).
+    # Duration: CUDA events around each engine launch on the library's stream.
+    eng_launches = max(1, rep.timings.engine_launches)
+    eng_ns_per_launch = rep.timings.engine_ns / eng_launches
+    eng_bytes_per_launch = (n + rep.stats.transfers_applied) * k * 4 / eng_launches
+    engine_gbs = eng_bytes_per_launch / max(eng_ns_per_launch, 1)
+    row_gbs = n * k * 4 / max(rep.timings.row_scan_ns, 1)
     rounds = rep.timings.relax_rounds
-    # engine algorithmic bytes: the (k x k+1) transfer-key graph read once per
-    # relaxation round (4 B/edge) + one cost row per arrival (4k B)
-    engine_bytes = rounds * k1 * 4 + n * k * 4
-    engine_gbs = engine_bytes / max(engine_ns, 1) / 1.0
     line = {
         "metric": "asral_solve_time_s",
         "baseline_metric": BASELINE_METRIC,
@@ -256,15 +259,22 @@ def run_ours(a):
         "e2e": {"value": round(e2e_s, 4), "unit": "s", "h2d_bytes_per_step": int(n * k * 4),
                 "d2h_bytes_per_step": int(n * 4)},
         "gpu_launches": int(launches // a.steps),
-        "roofline": {"kernel": "asral_engine_kernel", "bound": "hbm",
-                     "achieved": round(engine_gbs, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(engine_gbs / peak, 5), "traffic": None,
-                     "note": f"peak {peak_kind}; grid-barrier latency bound "
-                             f"({rep.timings.grid_barriers} barriers, {rounds} relaxation rounds)"},
+        "roofline": {"kernel": "cluster_engine_kernel", "bound": "hbm",
+                     "achieved": round(engine_gbs, 3), "peak": peak, "unit": "GB/s",
+                     "frac": round(engine_gbs / peak, 6), "traffic": None,
+                     "launches_per_step": eng_launches,
+                     "ms_per_launch": round(eng_ns_per_launch / 1e6, 3),
+                     "share_of_step": round(rep.timings.engine_ns / max(rep.timings.device_ns, 1), 4),
+                     "note": f"peak {peak_kind} (MEASURED_PEAKS.json hbm_gbs); latency-bound: "
+                             f"{rep.timings.grid_barriers} cluster barriers, {rounds} relaxation "
+                             "rounds per solve; bytes = 4k per arrival + 4k per applied transfer"},
         "scan": {"kernel": "seg_argmin_kernel (build_index full-matrix scan)",
                  "ms": round(ms, 4), "achieved": round(scan_gbs, 1), "peak": peak, "unit": "GB/s",
                  "frac": round(scan_gbs / peak, 4), "bytes": nbytes,
                  "sharded_ms_incl_allreduce": round(shard_ms, 4), "sharded_ranks": world},
+        "arrival_scan": {"kernel": "row_argmin_kernel", "ms": round(rep.timings.row_scan_ns / 1e6, 4),
+                         "achieved": round(row_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(row_gbs / peak, 4), "bytes": n * k * 4},
         "host_wall_s_per_step": round(wall / a.steps, 4),
         "stats": {"cycle_refines": rep.stats.cycle_refine_calls,
                   "path_refines": rep.stats.path_refine_calls,
@@ -287,30 +297,38 @@ def _problem(host, cap, fam, off, par):
     return ProblemInstance.from_arrays(host, cap, fam, params)
 
 
-def cpu_sample(problem, budget_s, workers):
-    """Bounded sample of the reference's asral main loop on this host."""
+def cpu_sample(problem, budget_s):
+    """Bounded sample of the reference's asral main loop on this host: the
+    first arrivals of the instance, grown until the loop alone takes about
+    budget_s / 2. Sequential: the reference's para-ASRAL WorkerPool
+    (parallel.hpp:31-124) can lose its done_cv_ wake-up and hang (DESIGN.md
+    §6), so the stock single-threaded asral_solve loop is what is timed."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     lib, kind = pyoracle.reference(), "reference"
     if lib is None:
-        lib, kind, workers = pyoracle.oracle(), "port", 1
-    arrivals = 64
+        lib, kind = pyoracle.oracle(), "port"
+    arrivals = 16
     while True:
-        ns, done = lib.asral_sample(problem, arrivals, workers)
-        if ns / 1e9 >= budget_s / 4 or done >= problem.n:
+        ns, done, setup = lib.asral_sample(problem, arrivals, 1)
+        loop_s = (ns - setup) / 1e9
+        if loop_s >= budget_s / 2 or done >= problem.n:
             break
-        arrivals = int(arrivals * min(8.0, max(2.0, budget_s / 4 / max(ns / 1e9, 1e-3))))
-    per = ns / 1e9 / done
-    return kind, workers, per, done, ns / 1e9
+        arrivals = int(arrivals * min(8.0, max(1.5, budget_s / 2 / max(loop_s, 1e-3))))
+    # estimate of the whole solve: setup (arrival queue, empty index) + the
+    # loop's per-arrival rate over every arrival. A lower bound: later
+    # arrivals meet fuller transfer heaps and overloaded centers.
+    est = setup / 1e9 + loop_s / done * problem.n
+    return kind, 1, est, done, ns / 1e9, setup / 1e9
 
 
 def cpu_baseline(dev, a, host, cap, fam, off, par):
     try:
         problem = _problem(host, cap, fam, off, par)
-        kind, workers, per, done, secs = cpu_sample(problem, a.ref_seconds, 1)
-        return {"value": round(per * a.n, 1), "unit": "s", "cores": workers, "kind": kind,
-                "sample": f"first {done} of {a.n} arrivals of the same instance "
-                          f"({secs:.1f} s CPU), extrapolated linearly"}
+        kind, workers, est, done, secs, setup = cpu_sample(problem, a.ref_seconds)
+        return {"value": round(est, 1), "unit": "s", "cores": workers, "kind": kind,
+                "sample": f"first {done} of {a.n} arrivals of the same instance ({secs:.1f} s "
+                          f"incl. {setup:.1f} s setup), extrapolated linearly (lower bound)"}
     except Exception as e:  # keep the GPU line even if the host sample fails
         return {"value": None, "unit": "s", "cores": 1, "kind": "reference",
                 "sample": f"failed: {e}"}
@@ -327,12 +345,12 @@ def run_reference(a):
     cap, fam, off, par = dev.centers()
     dev.close()
     problem = _problem(host, cap, fam, off, par)
-    workers = os.cpu_count() or 1
     vals = []
     for step in range(a.warmup + a.steps):
-        kind, w, per, done, secs = cpu_sample(problem, a.ref_seconds / max(1, a.steps), workers)
+        budget = a.ref_seconds / max(1, a.steps) if step >= a.warmup else 1.0
+        kind, w, est, done, secs, setup = cpu_sample(problem, budget)
         if step >= a.warmup:
-            vals.append(per * a.n)
+            vals.append(est)
     v = round(statistics.mean(vals), 1)
     line = {"impl": "reference", "metric": "asral_solve_time_s", "value": v, "unit": "s",
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "higher_is_better": False,
@@ -340,8 +358,10 @@ def run_reference(a):
             "config": {"workload": "configs[1]: |D|=1M x |S|=1000", "n_demands": a.n,
                        "n_centers": a.k},
             "cpu_baseline": {"value": v, "unit": "s", "cores": w, "kind": kind,
-                             "sample": f"first {done} of {a.n} arrivals per step ({secs:.1f} s), "
-                                       "para-asral worker pool, extrapolated linearly"},
+                             "sample": f"first {done} of {a.n} arrivals per step ({secs:.1f} s "
+                                       f"incl. {setup:.1f} s setup), sequential asral loop "
+                                       "(para-ASRAL's pool can deadlock), extrapolated linearly "
+                                       "(lower bound)"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -102,6 +102,9 @@ typedef struct lbdd_solve_report {
   int64_t relax_rounds; /* synchronous relaxation rounds executed */
   int64_t grid_barriers; /* device-wide barriers executed by the engine */
   int64_t device_ns;     /* CUDA-event time of the whole solve on its stream */
+  int64_t engine_ns;     /* CUDA-event time of the arrival-loop engine kernel launches */
+  int64_t engine_launches; /* engine kernel launches in this solve */
+  int64_t row_scan_ns;   /* CUDA-event time of the arrival scan kernel (row_argmin) */
 } lbdd_solve_report;
 
 /* Opaque handle: one instance resident in HBM on one device. */

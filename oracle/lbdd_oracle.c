@@ -1015,7 +1015,8 @@ int lbdd_oracle_arrival_queue(const lbdd_instance_desc* desc, int32_t* best_cent
 }
 
 int lbdd_oracle_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrivals,
-                             int32_t workers, int64_t* elapsed_ns, int64_t* arrivals_done) {
+                             int32_t workers, int64_t* elapsed_ns, int64_t* arrivals_done,
+                             int64_t* setup_ns) {
   (void)workers; /* the port is single-threaded */
   ENTRY_BEGIN
   const Inst I = inst_from(desc);
@@ -1024,6 +1025,7 @@ int lbdd_oracle_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrival
   State st;
   state_init(&st, &I);
   Arrival* q = build_arrivals(&I);
+  *setup_ns = now_ns() - t0;
   int64_t m = max_arrivals < I.n ? max_arrivals : I.n;
   for (int64_t i = 0; i < m; ++i) asral_arrival(&st, &q[i], 0);
   *elapsed_ns = now_ns() - t0;

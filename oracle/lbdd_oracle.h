@@ -62,7 +62,8 @@ int lbdd_oracle_generate(uint64_t seed, int64_t n, double ratio, double theta,
  * baseline sample); returns elapsed ns of the sampled loop. */
 int lbdd_oracle_asral_sample(const lbdd_instance_desc* desc,
                              int64_t max_arrivals, int32_t workers,
-                             int64_t* elapsed_ns, int64_t* arrivals_done);
+                             int64_t* elapsed_ns, int64_t* arrivals_done,
+                             int64_t* setup_ns);
 
 #ifdef __cplusplus
 }

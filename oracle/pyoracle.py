@@ -164,13 +164,16 @@ class CLib:
         return bc, bcost, order
 
     def asral_sample(self, inst, max_arrivals, workers=1):
-        """Time the first `max_arrivals` arrivals of asral_solve's main loop."""
+        """Time the first `max_arrivals` arrivals of asral_solve's main loop.
+        Returns (elapsed ns incl. setup, arrivals done, setup ns = arrival
+        queue + empty index)."""
         h = DescHolder(inst)
         ns = C.c_int64()
         done = C.c_int64()
+        setup = C.c_int64()
         self._check(self._fn("asral_sample")(h.ref, C.c_int64(max_arrivals), C.c_int32(workers),
-                                             C.byref(ns), C.byref(done)))
-        return ns.value, done.value
+                                             C.byref(ns), C.byref(done), C.byref(setup)))
+        return ns.value, done.value, setup.value
 
     def oracle_solve(self, inst, strict, size_limit=2000):
         """Reference-only: exact min-cost-flow optimum (oracle.hpp:144)."""

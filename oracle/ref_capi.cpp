@@ -352,7 +352,8 @@ extern "C" {
 // solver.hpp:135-167 verbatim in structure, stopped after `max_arrivals`
 // arrivals (no finish_report). Uses only the reference's own types.
 int lbdd_ref_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrivals,
-                          int32_t workers, int64_t* elapsed_ns, int64_t* arrivals_done) {
+                          int32_t workers, int64_t* elapsed_ns, int64_t* arrivals_done,
+                          int64_t* setup_ns) {
   return guarded([&] {
     const auto inst = to_instance(desc);
     lbdd::require_valid_instance(inst);
@@ -364,6 +365,8 @@ int lbdd_ref_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrivals,
     lbdd::SolverState st(inst);
     st.engine = scope.engine;
     auto queue = lbdd::detail::build_arrival_queue(inst);
+    *setup_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                    std::chrono::steady_clock::now() - start).count();
     int64_t done = 0;
     while (!queue.empty() && done < max_arrivals) {
       const auto [cost, d, s] = queue.top();

@@ -76,6 +76,9 @@ class SolveReportC(C.Structure):
         ("relax_rounds", C.c_int64),
         ("grid_barriers", C.c_int64),
         ("device_ns", C.c_int64),
+        ("engine_ns", C.c_int64),
+        ("engine_launches", C.c_int64),
+        ("row_scan_ns", C.c_int64),
     ]
 
 

@@ -137,6 +137,14 @@ struct lbdd_b200_instance {
   DevBuf<int64_t> MX;
   DevBuf<uint8_t> LN;
   int cluster_size = 0;  // chosen once per instance
+  // CUDA-event kernel times of the current solve (reported per solve)
+  int64_t engine_ns = 0, engine_launches = 0, row_scan_ns = 0;
+  cudaEvent_t kev[2] = {nullptr, nullptr};
+  float time_since(cudaEvent_t start) {  // kev[1] recorded + synced by the caller
+    float ms = 0;
+    cudaEventElapsedTime(&ms, start, kev[1]);
+    return ms;
+  }
   DevBuf<EngineCtl> ctl;
   DevBuf<GridBar> bar;
   DevBuf<PathEdge> path;
@@ -168,6 +176,8 @@ struct lbdd_b200_instance {
     ib_cnt.release(); ib_off.release(); ib_cursor.release(); ib_sorted.release();
     ib_pc.release(); ib_poff.release(); ib_bad.release(); obj_acc.release();
     obj_missing.release();
+    if (kev[0]) cudaEventDestroy(kev[0]);
+    if (kev[1]) cudaEventDestroy(kev[1]);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -305,6 +315,13 @@ void check_device_range(const lbdd_b200_instance* I) {
 
 // Arrival scan + sort (build_arrival_queue, solver.hpp:89-96), with the
 // matrix half of validate_instance. Returns device time in ns.
+void ensure_kernel_events(lbdd_b200_instance* I) {
+  if (I->kev[0] == nullptr) {
+    CUDA_OK(cudaEventCreate(&I->kev[0]));
+    CUDA_OK(cudaEventCreate(&I->kev[1]));
+  }
+}
+
 int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
   const int64_t n = I->n;
   I->best_center.ensure(n);
@@ -319,12 +336,16 @@ int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
   CUDA_OK(cudaMemcpyAsync(I->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
   const int blocks = static_cast<int>(std::min<int64_t>((n + 7) / 8, I->num_sms * 8));
   g_launches++;
+  ensure_kernel_events(I);
+  CUDA_OK(cudaEventRecord(I->kev[0], I->stream));
   row_argmin_kernel<<<std::max(blocks, 1), 256, 0, I->stream>>>(
       I->d_cm, I->pitch, n, static_cast<int32_t>(I->k), I->best_center.p, I->keys.p, I->minmax.p);
   CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaEventRecord(I->kev[1], I->stream));
   int64_t mm[2];
   CUDA_OK(cudaMemcpyAsync(mm, I->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, I->stream));
   CUDA_OK(cudaStreamSynchronize(I->stream));
+  I->row_scan_ns += static_cast<int64_t>(static_cast<double>(I->time_since(I->kev[0])) * 1e6);
   I->min_cost = mm[0];
   I->max_cost = mm[1];
   if (validate_matrix && I->min_cost <= 0)
@@ -627,11 +648,16 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
     A.a_end = std::min(a_end, a + chunk);
     void* args[] = {&A, &dumflag};
     g_launches++;
+    ensure_kernel_events(I);
+    CUDA_OK(cudaEventRecord(I->kev[0], I->stream));
     CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(asral_engine_kernel), dim3(L.grid),
                                         dim3(L.block), args, L.smem, I->stream));
     CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaEventRecord(I->kev[1], I->stream));
     CUDA_OK(cudaMemcpyAsync(&ctl, I->ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, I->stream));
     CUDA_OK(cudaStreamSynchronize(I->stream));
+    I->engine_ns += static_cast<int64_t>(static_cast<double>(I->time_since(I->kev[0])) * 1e6);
+    I->engine_launches += 1;
     if (ctl.error) raise_engine_error(ctl.error);
     A.search_base = ctl.search_count;
     a = A.a_end;
@@ -736,9 +762,14 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
     A.bk_ids = I->ib_sorted.p;
     CUDA_OK(cudaMemsetAsync(I->log_n.p, 0, sizeof(int32_t), I->stream));
     g_launches++;
+    ensure_kernel_events(I);
+    CUDA_OK(cudaEventRecord(I->kev[0], I->stream));
     CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, A, pi, dirty));
+    CUDA_OK(cudaEventRecord(I->kev[1], I->stream));
     CUDA_OK(cudaMemcpyAsync(&ctl, I->ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, I->stream));
     CUDA_OK(cudaStreamSynchronize(I->stream));
+    I->engine_ns += static_cast<int64_t>(static_cast<double>(I->time_since(I->kev[0])) * 1e6);
+    I->engine_launches += 1;
     g_err_arg = ctl.error_arg;
     if (ctl.error) {
       if (std::getenv("LBDD_B200_DEBUG") != nullptr)
@@ -1179,6 +1210,7 @@ lbdd_status lbdd_b200_solve(lbdd_b200_instance* inst, int32_t solver,
   return guarded([&] {
     CUDA_OK(cudaSetDevice(inst->device));
     std::memset(report, 0, sizeof(*report));
+    inst->engine_ns = inst->engine_launches = inst->row_scan_ns = 0;
     cudaEvent_t e0, e1;
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
@@ -1197,6 +1229,9 @@ lbdd_status lbdd_b200_solve(lbdd_b200_instance* inst, int32_t solver,
     float ms = 0;
     CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
     report->device_ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+    report->engine_ns = inst->engine_ns;
+    report->engine_launches = inst->engine_launches;
+    report->row_scan_ns = inst->row_scan_ns;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   });

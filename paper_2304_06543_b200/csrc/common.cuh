@@ -20,7 +20,7 @@
 
 // threads per CTA of the cluster engine (cluster.cu)
 #ifndef LBDD_CLUSTER_THREADS
-#define LBDD_CLUSTER_THREADS 256
+#define LBDD_CLUSTER_THREADS 512
 #endif
 
 #include <cstdint>

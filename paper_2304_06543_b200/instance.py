@@ -179,6 +179,9 @@ class PhaseTimings:
     relax_rounds: int = 0
     grid_barriers: int = 0
     device_ns: int = 0
+    engine_ns: int = 0
+    engine_launches: int = 0
+    row_scan_ns: int = 0
 
     def other_ns(self) -> int:
         return max(0, self.total_ns - self.index_update_ns - self.bellman_ford_ns)
@@ -204,6 +207,7 @@ class SolveReport:
                            rep.refinement_gain, rep.transfers_applied, rep.invariant_checks)
         tim = PhaseTimings(rep.index_update_ns, rep.bellman_ford_ns, rep.total_ns,
                            rep.scan_ns, rep.relax_rounds, rep.grid_barriers,
-                           rep.device_ns)
+                           rep.device_ns, rep.engine_ns, rep.engine_launches,
+                           rep.row_scan_ns)
         return SolveReport(_abi.SOLVER_NAMES.get(rep.solver, "?"), rep.objective, assignment,
                            load, stats, tim, rep.strict_surcharge, bool(rep.has_dummy_center))

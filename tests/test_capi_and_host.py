@@ -49,15 +49,17 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "lbdd_b200.h"\n'
-                   'int main(void){printf("%zu %zu %zu %zu", sizeof(lbdd_instance_desc),'
+                   'int main(void){printf("%zu %zu %zu %zu %zu", sizeof(lbdd_instance_desc),'
                    'sizeof(lbdd_solver_options), sizeof(lbdd_solve_report),'
-                   'offsetof(lbdd_solve_report, device_ns));return 0;}\n')
+                   'offsetof(lbdd_solve_report, device_ns), offsetof(lbdd_solve_report, row_scan_ns));'
+                   'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
                                             check=True).stdout.split()]
     assert sizes == [ctypes.sizeof(_abi.InstanceDesc), ctypes.sizeof(_abi.SolverOptionsC),
-                     ctypes.sizeof(_abi.SolveReportC), _abi.SolveReportC.device_ns.offset]
+                     ctypes.sizeof(_abi.SolveReportC), _abi.SolveReportC.device_ns.offset,
+                     _abi.SolveReportC.row_scan_ns.offset]
 
 
 def test_penalty_semantics():  # core.hpp:60-95

@@ -120,7 +120,8 @@ int main(int argc, char** argv) {
     compare(lbdd::greedy_solve(inst), lbdd::b200::greedy_solve(inst), "greedy " + std::to_string(c));
     // para-asral: the reference's WorkerPool (parallel.hpp:31-124) can lose
     // the done_cv_ wake-up in run() and hang, so its result is taken from
-    // the sequential solver, which it must equal (parallel_test.cpp)
+    // the sequential solver, which it must equal (parallel_test.cpp); the
+    // lost wake-up: drain() notifies done_cv_ without the mutex (parallel.hpp:91-92)
     lbdd::SolverOptions par;
     par.parallel = true;
     par.parallel_config.workers = 4;

@@ -668,8 +668,8 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
 // ---- the cluster engine (cluster.cu): one thread-block cluster ----
 size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
   return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * s + 2 * sizeof(cl::Pub) + 8 * 16 +
-         sizeof(cl::Pub) * cl::kMaxCS + 8 * (k + 1) +
-         4 * (cl::kMaxCS + 2) + 4 * static_cast<size_t>(cl::kMaxCS) * s + 4 * 2 * cl::kMaxSeg +
+         2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) + 8 * (k + 1) +
+         4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * static_cast<size_t>(cl::kMaxCS) * s + 4 * 2 * cl::kMaxSeg +
          8 * 16 + 8 * 16 +
          sizeof(PathEdge) * (k + 1) + 8 * block + 4 * 16 +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
@@ -742,7 +742,8 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
   EngineCtl ctl;
   // chunks of arrivals per launch: the bucket index is rebuilt in between,
   // so the move log a launch appends stays short
-  const int64_t chunk = 4096;
+  const char* ch = std::getenv("LBDD_B200_CHUNK");
+  const int64_t chunk = ch != nullptr ? std::max<int64_t>(64, std::atoll(ch)) : 4096;
   constexpr int32_t kLogCap = 1 << 16;
   I->log_d.ensure(kLogCap);
   I->log_to.ensure(kLogCap);

@@ -71,6 +71,14 @@ struct Pub {          // per-CTA published scalars of one exchange
   int64_t omin;       // smallest open label (held back or pushed this round)
 };
 
+struct Agg {          // cluster-wide reductions of the last exchange (warp 0)
+  int32_t pending;    // sum of Pub::pending
+  int32_t pad;
+  int64_t pmin;       // min Pub::pmin
+  int64_t omin;       // min Pub::omin
+  int64_t sinklab;    // min Pub::sinklab
+};
+
 struct CS {           // shared-memory layout of one CTA
   int64_t* lab;       // [s]
   int64_t* pis;       // [s]
@@ -82,11 +90,13 @@ struct CS {           // shared-memory layout of one CTA
   int32_t* qs;        // [blockDim]
   int32_t* misc;      // [16]: 0 queue count, 1 local count, 2 local err
   int64_t* red;       // [16] reduction scratch
-  Pub* all;           // [kMaxCS] snapshot of every CTA's pub after a barrier
+  Pub* all;           // every CTA's pub of the last exchange (= allb[par])
+  Pub* allb[2];       // [kMaxCS] each: pubs PUSHED by every CTA, by parity
+  Agg* agg;           // [1] reductions over all[] (computed once per exchange)
 
   int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
   int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
-  int32_t* idx;       // [kMaxCS * s] inbox slot of every pushed entry
+  FEntry* cmp;        // [kMaxCS * s] the pushed entries, compacted by the exchange
   int32_t* seg;       // [2 * kMaxSeg] rescan segments (slot, prefix end)
   int64_t* dbg;       // [16] instrumentation counters
   int64_t* prof;      // [16] lead-thread cycle counters per phase
@@ -101,13 +111,17 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.pis = reinterpret_cast<int64_t*>(p); p += 8 * s;
   S.inbox[0] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * kMaxCS * s;
   S.inbox[1] = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * kMaxCS * s;
+  S.cmp = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * static_cast<size_t>(kMaxCS) * s;
   S.pub[0] = reinterpret_cast<Pub*>(p); p += sizeof(Pub);
   S.pub[1] = reinterpret_cast<Pub*>(p); p += sizeof(Pub);
   S.red = reinterpret_cast<int64_t*>(p); p += 8 * 16;
-  S.all = reinterpret_cast<Pub*>(p); p += sizeof(Pub) * kMaxCS;
+  S.allb[0] = reinterpret_cast<Pub*>(p); p += sizeof(Pub) * kMaxCS;
+  S.allb[1] = reinterpret_cast<Pub*>(p); p += sizeof(Pub) * kMaxCS;
+  S.all = S.allb[0];
+  S.agg = reinterpret_cast<Agg*>(p); p += sizeof(Agg);
+
   S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
   S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
-  S.idx = reinterpret_cast<int32_t*>(p); p += 4 * static_cast<size_t>(kMaxCS) * s;
   S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 2 * kMaxSeg;
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
@@ -272,6 +286,24 @@ __device__ __forceinline__ bool list_insert(TopK& t, int64_t v) {
   if (t.len < kTopK) ++t.len;
   return p == 0;
 }
+// Concurrent rescan insert into an emptied list (all of M, MX start at
+// kEmpty): atomicMin at slot 0, the larger value carries on to the next
+// slot, an equal value (the same demand found twice: bucket and move log)
+// stops. Slots only decrease, so a value dropped past slot 3 is never among
+// the four smallest; the prefilter reads slot 3 at L2 (a stale larger value
+// only costs the cascade).
+__device__ __forceinline__ void list_sink(const EngineArgs& A, int64_t idx, int64_t x) {
+  int64_t* mx = A.MX + idx * 3;
+  if (x >= static_cast<int64_t>(__ldcg(reinterpret_cast<const long long*>(mx + 2)))) return;
+  int64_t old = atomicMin(reinterpret_cast<long long*>(&A.M[idx]), static_cast<long long>(x));
+  if (old == x) return;
+  x = max(old, x);
+  for (int i = 0; i < kTopK - 1 && x != kEmpty; ++i) {
+    old = atomicMin(reinterpret_cast<long long*>(&mx[i]), static_cast<long long>(x));
+    if (old == x) return;
+    x = max(old, x);
+  }
+}
 // returns 0 when the demand is not listed, else 4 | (1 when the head
 // changed) | (2 when a rescan is needed)
 __device__ __forceinline__ int list_remove(TopK& t, int32_t demand) {
@@ -362,16 +394,27 @@ __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
 // and par flips, so inbox[par ^ 1] holds the sources of the next relaxation.
 __device__ __forceinline__ void exchange(Ctx& X) {
   CS& S = X.S;
-  if (threadIdx.x == 0) S.pub[X.par]->err = S.misc[2];
-  X.cluster.sync();
   if (threadIdx.x < 32) {
-    // warp 0: fetch every CTA's pub, scan the counts, OR the errors
+    // warp 0 pushes this CTA's pub (written by thread 0) into slot `rank`
+    // of every CTA's allb[par] before the barrier, so that afterwards every
+    // read is local. A CTA can push for the next exchange only after this
+    // barrier, and by then every CTA has read allb[par ^ 1] for the last
+    // time (it did so before arriving here).
+    if (threadIdx.x == 0) S.pub[X.par]->err = S.misc[2];
+    __syncwarp();
+    if (threadIdx.x < X.csz) {
+      Pub* dst = X.cluster.map_shared_rank(S.allb[X.par], static_cast<int>(threadIdx.x));
+      dst[X.rank] = *S.pub[X.par];
+    }
+  }
+  X.cluster.sync();
+  S.all = S.allb[X.par];
+  if (threadIdx.x < 32) {
+    // warp 0: scan the counts, OR the errors
     const int lane = threadIdx.x;
     int c = 0, e = 0;
     if (lane < X.csz) {
-      const Pub* rp = X.cluster.map_shared_rank(S.pub[X.par], lane);
-      const Pub p = *rp;
-      S.all[lane] = p;
+      const Pub& p = S.all[lane];
       c = (p.count >= 0 && p.count <= X.s) ? p.count : 0;
       e = p.err;
     }
@@ -385,6 +428,29 @@ __device__ __forceinline__ void exchange(Ctx& X) {
     if (lane == 0) S.pref[0] = 0;
     const unsigned anyerr = __ballot_sync(0xffffffffu, e != 0);
     if (lane == 0) S.misc[4] = anyerr != 0;
+    // the reductions every thread used to recompute from all[] each round
+    int pend = 0;
+    long long pmin = kLabInf, omin = kLabInf, slab = kLabInf;
+    if (lane < X.csz) {
+      const Pub& p = S.all[lane];
+      pend = p.pending;
+      pmin = p.pmin;
+      omin = p.omin;
+      slab = p.sinklab;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pend += __shfl_xor_sync(0xffffffffu, pend, o);
+      pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+      omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
+      slab = min(slab, __shfl_xor_sync(0xffffffffu, slab, o));
+    }
+    if (lane == 0) {
+      S.agg->pending = pend;
+      S.agg->pmin = pmin;
+      S.agg->omin = omin;
+      S.agg->sinklab = slab;
+    }
   }
   if (X.lead) X.n_barriers += 1;
   __syncthreads();
@@ -396,7 +462,7 @@ __device__ __forceinline__ void exchange(Ctx& X) {
       const int mid = (lo + hi) >> 1;
       if (S.pref[mid] <= g) lo = mid; else hi = mid;
     }
-    S.idx[g] = lo * X.s + (g - S.pref[lo]);
+    S.cmp[g] = S.inbox[X.par][lo * X.s + (g - S.pref[lo])];
   }
   X.err |= S.misc[4];
   __syncthreads();
@@ -405,25 +471,16 @@ __device__ __forceinline__ void exchange(Ctx& X) {
   X.par ^= 1;
 }
 
-__device__ __forceinline__ int total_pending(const Ctx& X) {
-  int t = 0;
-  for (int r = 0; r < X.csz; ++r) t += X.S.all[r].pending;
-  return t;
-}
+__device__ __forceinline__ int total_pending(const Ctx& X) { return X.S.agg->pending; }
 // next threshold: at least Δ above the smallest held-back label
 __device__ __forceinline__ void advance_threshold(Ctx& X) {
   if (total_pending(X) == 0) return;
-  int64_t m = kLabInf;
-  for (int r = 0; r < X.csz; ++r) m = min(m, X.S.all[r].pmin);
+  const int64_t m = X.S.agg->pmin;
   const int64_t t = m > kLabInf - X.delta ? kLabInf : m + X.delta;
   if (t > X.T) X.T = t;
 }
 
-__device__ __forceinline__ int total_count(const Ctx& X) {
-  int t = 0;
-  for (int r = 0; r < X.csz; ++r) t += X.S.all[r].count;
-  return t;
-}
+__device__ __forceinline__ int total_count(const Ctx& X) { return X.S.pref[X.csz]; }
 
 // Push this CTA's changed nodes (and clear the flags) into every CTA's
 // inbox[par] (slot range rank * s): DSMEM stores, ordered before the
@@ -490,7 +547,6 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
   const EngineArgs& A = X.A;
   const int ns = X.v1 - X.v0;
   if (ns <= 0) return;  // uniform within the CTA
-  const FEntry* inbox = S.inbox[X.par ^ 1];  // pushed before the last exchange
   const int cpp = ns < static_cast<int>(blockDim.x) ? ((ns + 31) & ~31) : blockDim.x;
   const int rpp = blockDim.x / cpp;
   const int tx = threadIdx.x % cpp;
@@ -506,19 +562,43 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
     const int64_t bound = sinkcol ? bound_sink : bound_mid;
     int64_t best = kLabInf;
     const int cnt = S.pref[X.csz];
-    const int32_t* idx = S.idx;
+    const FEntry* cmp = S.cmp;
     if (sinkcol) {
       for (int t = ty; t < cnt; t += rpp) {
-        const FEntry e = inbox[idx[t]];
+        const FEntry e = cmp[t];
         const int64_t w = S.sinkw[fe_node(e)];  // kNoEdge for the anchor itself
         if (w == kNoEdge) continue;
         const int64_t cand = e.lp + w * kUnit + base;
         if (cand < bound && cand < best) best = cand;
       }
+    } else if (X.tile && X.A.dummies == nullptr) {
+      // asral: no placeholder flags. cand < min(bound, best) is tested as
+      // lp + w * unit < lim with lim = min(bound, best) - base, shrinking
+      const int16_t* wcol = S.wt + col;
+      const int64_t lim0 = bound - base;
+      int64_t lim = lim0;
+      const int64_t sw = X.s;
+      int t = ty;
+      // four independent (entry, key) load pairs in flight per iteration
+      for (; t + 3 * rpp < cnt; t += 4 * rpp) {
+        const FEntry e0 = cmp[t], e1 = cmp[t + rpp], e2 = cmp[t + 2 * rpp], e3 = cmp[t + 3 * rpp];
+        const int16_t k0 = wcol[e0.nd * sw], k1 = wcol[e1.nd * sw];
+        const int16_t k2 = wcol[e2.nd * sw], k3 = wcol[e3.nd * sw];
+        if (k0 != kNoKey16 && e0.nd != v) lim = min(lim, e0.lp + static_cast<int64_t>(k0) * kUnit);
+        if (k1 != kNoKey16 && e1.nd != v) lim = min(lim, e1.lp + static_cast<int64_t>(k1) * kUnit);
+        if (k2 != kNoKey16 && e2.nd != v) lim = min(lim, e2.lp + static_cast<int64_t>(k2) * kUnit);
+        if (k3 != kNoKey16 && e3.nd != v) lim = min(lim, e3.lp + static_cast<int64_t>(k3) * kUnit);
+      }
+      for (; t < cnt; t += rpp) {
+        const FEntry e = cmp[t];
+        const int16_t key = wcol[e.nd * sw];
+        if (key != kNoKey16 && e.nd != v) lim = min(lim, e.lp + static_cast<int64_t>(key) * kUnit);
+      }
+      if (lim < lim0) best = lim + base;
     } else if (X.tile) {
 #pragma unroll 4
       for (int t = ty; t < cnt; t += rpp) {
-        const FEntry e = inbox[idx[t]];
+        const FEntry e = cmp[t];
         const int u = fe_node(e);
         const int64_t w = key16_weight(S.wt[static_cast<int64_t>(u) * X.s + col], fe_dum(e));
         if (u == v || w == kNoEdge) continue;
@@ -536,7 +616,7 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
           e[q].nd = -1;
           m[q] = kEmpty;
           if (tq < cnt) {
-            e[q] = inbox[idx[tq]];
+            e[q] = cmp[tq];
             m[q] = A.M[static_cast<int64_t>(fe_node(e[q])) * A.k + v];
           }
         }
@@ -582,11 +662,7 @@ __device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, 
 // min_open + sink_inc > S, nothing can change it or any node on its chain.
 __device__ __forceinline__ bool sink_settled(const Ctx& X, int64_t sink_inc) {
   if (sink_inc == kLabInf) return false;
-  int64_t sl = kLabInf, om = kLabInf;
-  for (int r = 0; r < X.csz; ++r) {
-    sl = min(sl, X.S.all[r].sinklab);
-    om = min(om, X.S.all[r].omin);
-  }
+  const int64_t sl = X.S.agg->sinklab, om = X.S.agg->omin;
   return sl != kLabInf && (om == kLabInf || om + sink_inc > sl);
 }
 
@@ -616,9 +692,7 @@ __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64
 }
 
 __device__ __forceinline__ int64_t sink_label(const Ctx& X) {
-  int64_t l = kLabInf;
-  for (int r = 0; r < X.csz; ++r) l = min(l, X.S.all[r].sinklab);
-  return l;
+  return X.S.agg->sinklab;
 }
 
 // Start a search: labels of owned nodes to +inf, π(anchor-in) := π(anchor).
@@ -859,10 +933,8 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   }
   if (threadIdx.x == 0) S.pub[X.par]->count = 0;
   PROF_MARK(X, 0);   // T1
-  // before the exchange: once past it, other CTAs' T3 rescans write M of
-  // any column
-  __syncthreads();
-  validate_lists(X, 3);
+  // (no list validation here: until this barrier the lead's home[] writes
+  // and, after it, other CTAs' T3 rescans race with a reader of the lists)
   exchange(X);
   PROF_MARK(X, 12);  // apply exchanges
   // ---- T3: rescans of the invalidated entries over the final buckets ----
@@ -935,7 +1007,8 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       __syncthreads();
       const int qn = S.misc[0];
       // (member, invalidated column) pairs spread over every thread: two
-      // independent cost loads and one atomicMin per pair
+      // independent cost loads, then the pair's transfer sinks into the
+      // entry's emptied top-4 list (M, MX) by an atomicMin cascade
       for (int p = threadIdx.x; p < qn * maxcnt; p += blockDim.x) {
         const int q = p % qn;
         const int xx = p / qn;
@@ -946,8 +1019,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
         const int u = S.path[sl2].from_center;
         const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
         const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
-        atomicMin(reinterpret_cast<long long*>(&A.M[static_cast<int64_t>(u) * k + j]),
-                  static_cast<long long>(pack_transfer(row[j] - row[u], d2)));
+        list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - row[u], d2));
       }
       __syncthreads();
     }
@@ -956,8 +1028,8 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   PROF_MARK(X, 13);  // T3
   exchange(X);
   PROF_MARK(X, 12);
-  // rescanned entries now hold their exact minimum: a one-element,
-  // incomplete list (or an empty complete one); refresh my tile columns
+  // rescanned entries now hold the (up to) four smallest transfers of their
+  // row: complete when fewer than four exist; refresh my tile columns
   for (int i = 0; i < len; ++i) {
     const PathEdge e = S.path[i];
     if (e.kind != kEdgeTransfer) continue;
@@ -967,7 +1039,9 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       if (j < jlo || j >= jhi) continue;
       const int64_t idx = static_cast<int64_t>(e.from_center) * k + j;
       const int64_t m = A.M[idx];
-      A.LN[idx] = m == kEmpty ? 8 : 1;
+      const int64_t* mx = A.MX + idx * 3;
+      const int len = (m != kEmpty) + (mx[0] != kEmpty) + (mx[1] != kEmpty) + (mx[2] != kEmpty);
+      A.LN[idx] = static_cast<uint8_t>(len | (len < kTopK ? 8 : 0));
       if (X.tile) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = key16(m);
     }
   }
@@ -1290,6 +1364,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       const int64_t refund = refund_penalty(X, s, A.load[s]);
       // C = min_{u != s} marginal(u) - refund + π(u) - π(s): the most a
       // penalty edge can subtract; prune the search to d_rc < -C
+      const int64_t pis_now = pi_of(X, s);
       int64_t lmin = kEmpty;
       for (int u = X.v0 + threadIdx.x; u < min(X.v1, k); u += blockDim.x) {
         if (u == s) continue;
@@ -1299,7 +1374,6 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       __syncthreads();
       atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(lmin));
       __syncthreads();
-      const int64_t pis_now = pi_of(X, s);
       if (threadIdx.x == 0) {
         S.pub[X.par]->val = S.red[0];
         S.pub[X.par]->count = 0;

@@ -121,7 +121,8 @@ long long lbdd_b200_launch_count(void);
  * those with an empty initial frontier, out[6..8] frontier entries relaxed,
  * out[9] path searches pruned by the penalty bound, out[10..12] rounds per
  * kind, out[13..15] path-bound statistics; out[16..31] cluster-engine
- * lead-thread cycles per phase. */
+ * lead-thread cycles per phase; out[32..37] rescans (calls, full scans,
+ * row-mode, candidates, members, member-column pairs). out has 40 slots. */
 void lbdd_b200_engine_counters(int64_t* out);
 
 /* Upload an instance (host arrays) to `device`. Replaces constructing a

@@ -47,6 +47,7 @@ constexpr int kMaxCS = 16;
 constexpr int kStage = 256;            // frontier entries staged per pass
 constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
 constexpr int kMaxSeg = 32;            // source rows rescanned per apply via the index
+constexpr int kRowSlots = 8;           // source rows of a row-mode rescan (column bitmaps)
 
 // A frontier entry as pushed into every CTA's inbox: the node (bit 31: a
 // surplus placeholder sits there, strict-mode edge rule) and its label with
@@ -88,6 +89,8 @@ struct CS {           // shared-memory layout of one CTA
   uint8_t* chg;       // [s]
   int32_t* qd;        // [blockDim] rescan queue
   int32_t* qs;        // [blockDim]
+  int32_t* qh;        // [blockDim] CM[d][home] of each queued member
+  uint32_t* bits;     // [kRowSlots * ceil(k / 32)] invalidated columns per rescan slot
   int32_t* misc;      // [16]: 0 queue count, 1 local count, 2 local err
   int64_t* red;       // [16] reduction scratch
   Pub* all;           // every CTA's pub of the last exchange (= allb[par])
@@ -128,6 +131,8 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
   S.qd = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
   S.qs = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
+  S.qh = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
+  S.bits = reinterpret_cast<uint32_t*>(p); p += 4 * static_cast<size_t>(kRowSlots) * ((k + 31) / 32);
   S.misc = reinterpret_cast<int32_t*>(p); p += 4 * 16;
   S.wt = reinterpret_cast<int16_t*>(p); p += tile ? 2 * static_cast<size_t>(k) * s : 0;
   S.chg = reinterpret_cast<uint8_t*>(p);
@@ -967,6 +972,33 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       if (S.path[i].kind == kEdgeTransfer) maxcnt = max(maxcnt, A.inv_cnt[i]);
     }
     const int64_t ncand = full ? A.n : nbase + nlog;
+    // row mode: when a slot invalidated a good part of its row, members'
+    // cost rows are streamed (coalesced 16 B pieces, one column bitmap per
+    // slot) instead of gathering one 4 B key per (member, column)
+    const int nv = (k + 3) >> 2;
+    const int nw32 = (k + 31) >> 5;
+    const bool rowmode = !full && nseg <= kRowSlots && 4 * maxcnt >= nv;
+    if (X.lead) {
+      A.ctl->resc[0] += 1;
+      A.ctl->resc[1] += full;
+      A.ctl->resc[2] += rowmode;
+      A.ctl->resc[3] += ncand;
+      int64_t pairs = 0;
+      for (int i = 0; i < len; ++i) pairs += (S.path[i].kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
+      A.ctl->resc[5] += pairs;
+    }
+    if (rowmode) {
+      for (int w = threadIdx.x; w < nseg * nw32; w += blockDim.x) S.bits[w] = 0;
+      __syncthreads();
+      for (int g = 0; g < nseg; ++g) {
+        const int sl = seg[2 * g];
+        const int cnt = A.inv_cnt[sl];
+        for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+          const int j = A.inv_cols[static_cast<int64_t>(sl) * k + x];
+          atomicOr(&S.bits[g * nw32 + (j >> 5)], 1u << (j & 31));
+        }
+      }
+    }
     const int64_t stride = static_cast<int64_t>(X.csz) * blockDim.x;
     for (int64_t base = static_cast<int64_t>(X.rank) * blockDim.x; base < ncand; base += stride) {
       if (threadIdx.x == 0) S.misc[0] = 0;
@@ -1002,10 +1034,39 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           const int q = atomicAdd(&S.misc[0], 1);
           S.qd[q] = dd;
           S.qs[q] = sl;
+          S.qh[q] = A.cm[static_cast<int64_t>(dd) * A.pitch + S.path[sl].from_center];
         }
       }
       __syncthreads();
       const int qn = S.misc[0];
+      if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&A.ctl->resc[4]),
+                                      static_cast<unsigned long long>(qn));
+      if (rowmode) {
+        // (member, 16 B piece) items: consecutive threads read consecutive
+        // pieces of one member's row
+        for (int p = threadIdx.x; p < qn * nv; p += blockDim.x) {
+          const int q = p / nv;
+          const int c4 = p - q * nv;
+          const int sl2 = S.qs[q];
+          int g = 0;
+          while (seg[2 * g] != sl2) ++g;
+          const uint32_t word = S.bits[g * nw32 + (c4 >> 3)] >> ((c4 & 7) * 4);
+          if ((word & 15u) == 0) continue;
+          const int32_t d2 = S.qd[q];
+          const int32_t hv = S.qh[q];
+          const int u = S.path[sl2].from_center;
+          const int4 x4 = reinterpret_cast<const int4*>(A.cm + static_cast<int64_t>(d2) * A.pitch)[c4];
+          const int32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (word & (1u << e)) {
+              list_sink(A, static_cast<int64_t>(u) * k + 4 * c4 + e, pack_transfer(xs[e] - hv, d2));
+            }
+          }
+        }
+        __syncthreads();
+        continue;
+      }
       // (member, invalidated column) pairs spread over every thread: two
       // independent cost loads, then the pair's transfer sinks into the
       // entry's emptied top-4 list (M, MX) by an atomicMin cascade
@@ -1019,7 +1080,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
         const int u = S.path[sl2].from_center;
         const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
         const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
-        list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - row[u], d2));
+        list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
       }
       __syncthreads();
     }

@@ -87,6 +87,8 @@ struct EngineCtl {
   int64_t barriers;               // grid barriers executed
   int64_t dbg[16];                // engine instrumentation (see capi)
   int64_t prof[16];               // cluster engine: lead-thread cycles per phase
+  int64_t resc[8];                // cluster engine rescans: calls, full-scan, row-mode,
+                                  // candidates, members, (member, column) pairs
   int32_t error;
   int32_t error_arg;
   int32_t prev_sources;           // transfer sources of the last applied path

@@ -191,3 +191,24 @@ def test_cpp_drop_in():
     out = subprocess.run([exe, "12"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "drop-in ok" in out.stdout
+
+
+@pytest.mark.parametrize("tile", ["1", "0"])
+def test_medium_solves_lists_rescans_and_key_paths(dev, oracle, tile, monkeypatch):
+    """Mid-size random instances through the cluster engine: top-4 transfer
+    lists, rescans over the bucket index + move log (LBDD_B200_CHUNK=64: many
+    launches, so buckets are rebuilt and the log restarts often), the int16
+    key tile (tile=1, narrow costs) and the global-key path (tile=0, or keys
+    wider than int16). Bit-exact against the oracle."""
+    monkeypatch.setenv("LBDD_B200_TILE", tile)
+    monkeypatch.setenv("LBDD_B200_CHUNK", "64")
+    rng = po.Mt19937_64(97 + int(tile))
+    for it in range(6):
+        n, k = 300 + rng() % 700, 20 + rng() % 140
+        max_cost = [100, 5000, 200000][it % 3]
+        inst = po.random_instance(rng, n=n, k=k, max_cost=max_cost, penalty_hi=max_cost // 2 + 1,
+                                  total_capacity=int(n * [0.8, 1.0, 0.6][it % 3]))
+        for solver in ["asral", "strict"]:
+            opts = SolverOptions(refine_to_fixpoint=bool(it % 2))
+            assert same_report(dev.solve(inst, solver, opts), oracle.solve(inst, solver, opts)), \
+                (it, solver, n, k, max_cost)

@@ -52,6 +52,17 @@ def parse():
     return p.parse_args()
 
 
+def engine_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one cluster_engine_kernel
+    launch (4096 arrivals) from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "engine_traffic.json")) as f:
+            t = json.load(f)
+        return int(t["dram_bytes_per_launch"]), t.get("source", "")
+    except Exception:
+        return None, ""
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -261,7 +272,8 @@ def run_ours(a):
         "gpu_launches": int(launches // a.steps),
         "roofline": {"kernel": "cluster_engine_kernel", "bound": "hbm",
                      "achieved": round(engine_gbs, 3), "peak": peak, "unit": "GB/s",
-                     "frac": round(engine_gbs / peak, 6), "traffic": None,
+                     "frac": round(engine_gbs / peak, 6), "traffic": engine_traffic()[0],
+                     "traffic_source": engine_traffic()[1],
                      "launches_per_step": eng_launches,
                      "ms_per_launch": round(eng_ns_per_launch / 1e6, 3),
                      "share_of_step": round(rep.timings.engine_ns / max(rep.timings.device_ns, 1), 4),

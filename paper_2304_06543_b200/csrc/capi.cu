@@ -668,7 +668,7 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
 // ---- the cluster engine (cluster.cu): one thread-block cluster ----
 size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
   return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * s + 2 * sizeof(cl::Pub) + 8 * 16 +
-         2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) * (block / 32) + 8 * (k + 1) +
+         2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) + 8 * (k + 1) +
          4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * static_cast<size_t>(cl::kMaxCS) * s + 4 * 2 * cl::kMaxSeg +
          8 * 16 + 8 * 16 +
          sizeof(PathEdge) * (k + 1) + 12 * block + 4 * 16 +
@@ -727,6 +727,8 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
     A.delta_step = ev != nullptr ? std::atoll(ev) : 1;
     const char* evp = std::getenv("LBDD_B200_DELTA_PATH");
     A.delta_path = evp != nullptr ? std::atoll(evp) : A.delta_step;
+    const char* pf = std::getenv("LBDD_B200_PROF");
+    A.profile = pf != nullptr && std::string(pf) == "1";
     const char* dc = std::getenv("LBDD_B200_CHECK");
     A.debug_checks = dc != nullptr && std::string(dc) == "1";
   }

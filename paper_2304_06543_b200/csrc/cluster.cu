@@ -72,9 +72,9 @@ struct Pub {          // per-CTA published scalars of one exchange
   int64_t omin;       // smallest open label (held back or pushed this round)
 };
 
-struct Agg {          // cluster-wide reductions of the last exchange (one copy per warp)
+struct Agg {          // cluster-wide reductions of the last exchange (warp 0)
   int32_t pending;    // sum of Pub::pending
-  int32_t count;      // sum of Pub::count (entries in cmp)
+  int32_t pad;
   int64_t pmin;       // min Pub::pmin
   int64_t omin;       // min Pub::omin
   int64_t sinklab;    // min Pub::sinklab
@@ -105,7 +105,7 @@ struct CS {           // shared-memory layout of one CTA
   int64_t* red;       // [16] reduction scratch
   Pub* all;           // every CTA's pub of the last exchange (= allb[par])
   Pair2<Pub> allb;     // [kMaxCS] each: pubs PUSHED by every CTA, by parity
-  Agg* agg;           // [warps] reductions over all[], each warp its own copy
+  Agg* agg;           // [1] reductions over all[] (computed once per exchange)
 
   int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
   int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
@@ -128,7 +128,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.red = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.allb = {reinterpret_cast<Pub*>(p), kMaxCS}; p += 2 * sizeof(Pub) * kMaxCS;
   S.all = S.allb[0];
-  S.agg = reinterpret_cast<Agg*>(p); p += sizeof(Agg) * (blockDim.x / 32);
+  S.agg = reinterpret_cast<Agg*>(p); p += sizeof(Agg);
 
   S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
   S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
@@ -146,10 +146,12 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   return S;
 }
 
-// lead-thread phase profiler: prof[i] += cycles since the last mark
+// lead-thread phase profiler: prof[i] += cycles since the last mark (only
+// with LBDD_B200_PROF=1: the marks sit on rank 0's critical path, which
+// every other CTA waits for at the next cluster barrier)
 #define PROF_MARK(X, i)                                      \
   do {                                                       \
-    if ((X).lead) {                                          \
+    if ((X).lead && (X).A.profile) {                         \
       const long long now__ = clock64();                     \
       (X).S.prof[i] += now__ - (X).S.prof[15];               \
       (X).S.prof[15] = now__;                                \
@@ -423,86 +425,78 @@ __device__ __forceinline__ void exchange(Ctx& X) {
   }
   X.cluster.sync();
   S.all = S.allb[X.par];
-  // every warp reduces the 16 pubs itself (lane r reads CTA r's slot), so
-  // no block barrier separates the reduction from its readers: each warp
-  // keeps its own copy of the aggregates (S.agg[warp])
-  const int lane = threadIdx.x & 31;
-  int c = 0, e = 0, pend = 0;
-  long long pmin = kLabInf, omin = kLabInf, slab = kLabInf;
-  if (lane < X.csz) {
-    const Pub& p = S.all[lane];
-    c = (p.count >= 0 && p.count <= X.s) ? p.count : 0;
-    e = p.err;
-    pend = p.pending;
-    pmin = p.pmin;
-    omin = p.omin;
-    slab = p.sinklab;
-  }
-  int incl = c;
+  if (threadIdx.x < 32) {
+    // warp 0: scan the counts, OR the errors
+    const int lane = threadIdx.x;
+    int c = 0, e = 0;
+    if (lane < X.csz) {
+      const Pub& p = S.all[lane];
+      c = (p.count >= 0 && p.count <= X.s) ? p.count : 0;
+      e = p.err;
+    }
+    int incl = c;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int excl = incl - c;
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  const unsigned anyerr = __ballot_sync(0xffffffffu, e != 0);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < X.csz) S.pref[lane + 1] = incl;
+    if (lane == 0) S.pref[0] = 0;
+    const unsigned anyerr = __ballot_sync(0xffffffffu, e != 0);
+    if (lane == 0) S.misc[4] = anyerr != 0;
+    // the reductions every thread used to recompute from all[] each round
+    int pend = 0;
+    long long pmin = kLabInf, omin = kLabInf, slab = kLabInf;
+    if (lane < X.csz) {
+      const Pub& p = S.all[lane];
+      pend = p.pending;
+      pmin = p.pmin;
+      omin = p.omin;
+      slab = p.sinklab;
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    pend += __shfl_xor_sync(0xffffffffu, pend, o);
-    pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
-    omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
-    slab = min(slab, __shfl_xor_sync(0xffffffffu, slab, o));
-  }
-  if (lane == 0) {
-    Agg* g = S.agg + (threadIdx.x >> 5);
-    g->pending = pend;
-    g->count = total;
-    g->pmin = pmin;
-    g->omin = omin;
-    g->sinklab = slab;
-  }
-  // collect's per-round scratch, read by thread 0 before the barrier and
-  // next written by collect after the block barrier below
-  if (threadIdx.x == 0) {
-    S.misc[1] = 0;
-    S.misc[3] = 0;
-    S.red[2] = kLabInf;
-    S.red[3] = kLabInf;
+    for (int o = 16; o > 0; o >>= 1) {
+      pend += __shfl_xor_sync(0xffffffffu, pend, o);
+      pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+      omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
+      slab = min(slab, __shfl_xor_sync(0xffffffffu, slab, o));
+    }
+    if (lane == 0) {
+      S.agg->pending = pend;
+      S.agg->pmin = pmin;
+      S.agg->omin = omin;
+      S.agg->sinklab = slab;
+    }
   }
   if (X.lead) X.n_barriers += 1;
-  // flat index of the pushed entries: entry g sits in the segment r with
-  // the largest excl[r] <= g (warp-uniform loop; shuffles, no shared scan)
-  for (int g0 = 0; g0 < total; g0 += blockDim.x) {
-    const int g = g0 + static_cast<int>(threadIdx.x);
-    int lo = 0, base = 0;
-    for (int r = 1; r < X.csz; ++r) {
-      const int er = __shfl_sync(0xffffffffu, excl, r);
-      if (er <= g) {
-        lo = r;
-        base = er;
-      }
+  __syncthreads();
+  // flat index of the pushed entries: slot of the g-th entry in the inbox
+  const int total = S.pref[X.csz];
+  for (int g = threadIdx.x; g < total; g += blockDim.x) {
+    int lo = 0, hi = X.csz;  // last r with pref[r] <= g
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (S.pref[mid] <= g) lo = mid; else hi = mid;
     }
-    if (g < total) S.cmp[g] = S.inbox[X.par][lo * X.s + (g - base)];
+    S.cmp[g] = S.inbox[X.par][lo * X.s + (g - S.pref[lo])];
   }
-  X.err |= anyerr != 0u;
+  X.err |= S.misc[4];
   __syncthreads();
   // the next phase writes the other buffer while slow CTAs may still read
   // this one; it is rewritten only after the next barrier
   X.par ^= 1;
 }
 
-__device__ __forceinline__ const Agg& agg(const Ctx& X) { return X.S.agg[threadIdx.x >> 5]; }
-__device__ __forceinline__ int total_pending(const Ctx& X) { return agg(X).pending; }
+__device__ __forceinline__ int total_pending(const Ctx& X) { return X.S.agg->pending; }
 // next threshold: at least Δ above the smallest held-back label
 __device__ __forceinline__ void advance_threshold(Ctx& X) {
   if (total_pending(X) == 0) return;
-  const int64_t m = agg(X).pmin;
+  const int64_t m = X.S.agg->pmin;
   const int64_t t = m > kLabInf - X.delta ? kLabInf : m + X.delta;
   if (t > X.T) X.T = t;
 }
 
-__device__ __forceinline__ int total_count(const Ctx& X) { return agg(X).count; }
+__device__ __forceinline__ int total_count(const Ctx& X) { return X.S.pref[X.csz]; }
 
 // Push this CTA's changed nodes (and clear the flags) into every CTA's
 // inbox[par] (slot range rank * s): DSMEM stores, ordered before the
@@ -524,52 +518,28 @@ __device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label
 // stay pending (their flag kept) and report their count and minimum.
 __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor) {
   CS& S = X.S;
-  // misc[1], misc[3], red[2], red[3] were reset by the last exchange.
-  // Warp-uniform loop: the improved nodes of a warp get consecutive inbox
-  // slots (one atomicAdd per warp) and each is pushed by 16 lanes at once,
-  // lane r storing into CTA r's inbox.
-  const int lane = threadIdx.x & 31;
-  const int ns = X.v1 - X.v0;
-  for (int i0 = 0; i0 < ns; i0 += blockDim.x) {
-    const int i = i0 + static_cast<int>(threadIdx.x);
-    bool push = false;
-    int32_t nd = 0;
-    int64_t lp = 0;
-    if (i < ns && S.chg[i]) {
-      const int v = X.v0 + i;
-      if (v == X.k) {
-        S.chg[i] = 0;  // anchor-in has no out-edges
-      } else {
-        const int64_t label = S.lab[i];
-        if (label > X.T) {
-          atomicAdd(&S.misc[3], 1);
-          atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
-        } else {
-          S.chg[i] = 0;
-          atomicMin(reinterpret_cast<long long*>(&S.red[3]), static_cast<long long>(label));
-          push = true;
-          nd = v | ((kind != kPath && has_dummy(X, v)) ? static_cast<int32_t>(0x80000000u) : 0);
-          lp = label + S.pis[i] * (int64_t(1) << kCandShift);
-          if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
-        }
-      }
+  if (threadIdx.x == 0) {
+    S.misc[1] = 0;
+    S.misc[3] = 0;
+    S.red[2] = kLabInf;
+    S.red[3] = kLabInf;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    if (!S.chg[i]) continue;
+    const int v = X.v0 + i;
+    if (v == X.k) { S.chg[i] = 0; continue; }  // anchor-in has no out-edges
+    const int64_t label = S.lab[i];
+    if (label > X.T) {
+      atomicAdd(&S.misc[3], 1);
+      atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
+      continue;
     }
-    unsigned m = __ballot_sync(0xffffffffu, push);
-    if (m == 0u) continue;
-    int pos = 0;
-    if (lane == 0) pos = atomicAdd(&S.misc[1], __popc(m));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    FEntry* box = X.cluster.map_shared_rank(S.inbox[X.par], lane < X.csz ? lane : 0) + X.rank * X.s;
-    while (m != 0u) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      FEntry e;
-      e.nd = __shfl_sync(0xffffffffu, nd, src);
-      e.pad = 0;
-      e.lp = __shfl_sync(0xffffffffu, lp, src);
-      if (lane < X.csz) box[pos] = e;
-      ++pos;
-    }
+    S.chg[i] = 0;
+    atomicMin(reinterpret_cast<long long*>(&S.red[3]), static_cast<long long>(label));
+    const int pos = atomicAdd(&S.misc[1], 1);
+    push_entry(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
+    if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -604,7 +574,7 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
     const int64_t base = 1 - S.pis[col] * kUnit;  // candidate = lp + w*unit + base
     const int64_t bound = sinkcol ? bound_sink : bound_mid;
     int64_t best = kLabInf;
-    const int cnt = total_count(X);
+    const int cnt = S.pref[X.csz];
     const FEntry* cmp = S.cmp;
     if (sinkcol) {
       for (int t = ty; t < cnt; t += rpp) {
@@ -705,7 +675,7 @@ __device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, 
 // min_open + sink_inc > S, nothing can change it or any node on its chain.
 __device__ __forceinline__ bool sink_settled(const Ctx& X, int64_t sink_inc) {
   if (sink_inc == kLabInf) return false;
-  const int64_t sl = agg(X).sinklab, om = agg(X).omin;
+  const int64_t sl = X.S.agg->sinklab, om = X.S.agg->omin;
   return sl != kLabInf && (om == kLabInf || om + sink_inc > sl);
 }
 
@@ -735,7 +705,7 @@ __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64
 }
 
 __device__ __forceinline__ int64_t sink_label(const Ctx& X) {
-  return agg(X).sinklab;
+  return X.S.agg->sinklab;
 }
 
 // Start a search: labels of owned nodes to +inf, π(anchor-in) := π(anchor).
@@ -1328,8 +1298,6 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   }
   if (threadIdx.x < 16) S.misc[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
-    S.red[2] = kLabInf;
-    S.red[3] = kLabInf;
     for (int b = 0; b < 2; ++b) {
       S.pub[b]->count = 0;
       S.pub[b]->err = 0;

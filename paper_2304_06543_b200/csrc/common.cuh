@@ -153,6 +153,7 @@ struct EngineArgs {
   int32_t pad2;
   int64_t delta_step;    // cluster engine Δ-stepping width (cost units, <= 0: off)
   int64_t delta_path;    // Δ of the penalty-path searches (cost units, <= 0: off)
+  int32_t profile;       // lead-thread phase cycle counters (LBDD_B200_PROF=1)
   // bucket index (demands grouped by home, built before each launch) and
   // the move log appended since; nullptr: rescans scan every demand
   const int32_t* bk_off;  // k + 1

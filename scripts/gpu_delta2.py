@@ -4,7 +4,7 @@ import os, sys, subprocess
 n = int(sys.argv[1]); k = int(sys.argv[2])
 for spec in sys.argv[3:]:
     d, dp, *ch = spec.split(",")
-    env = dict(os.environ, LBDD_B200_DELTA=d, LBDD_B200_DELTA_PATH=dp, LBDD_B200_PROF="1")
+    env = dict(os.environ, LBDD_B200_DELTA=d, LBDD_B200_DELTA_PATH=dp, LBDD_B200_PROF=os.environ.get("LBDD_B200_PROF", "1"))
     if ch:
         env["LBDD_B200_CHUNK"] = ch[0]
     out = subprocess.run([sys.executable, "-c", f"""

@@ -676,6 +676,14 @@ size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
 }
 
+bool cluster_engine_fits(int k) {
+  for (int cs : {16, 8, 4, 2, 1}) {
+    const int s = (k + 1 + cs - 1) / cs;
+    if (cluster_smem_bytes(k, s, LBDD_CLUSTER_THREADS, false) <= 220 * 1024) return true;
+  }
+  return false;
+}
+
 bool use_grid_engine() {
   const char* e = std::getenv("LBDD_B200_ENGINE");
   return e != nullptr && std::string(e) == "grid";
@@ -795,8 +803,11 @@ EngineCtl run_solver_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin
                             bool keys16) {
   const char* e = std::getenv("LBDD_B200_TILE");
   if (e != nullptr && std::string(e) == "0") keys16 = false;
-  return use_grid_engine() ? run_engine(I, A, a_begin, a_end)
-                           : run_cluster_engine(I, A, a_begin, a_end, keys16);
+  // the one-cluster engine keeps O(k) per-CTA state in shared memory; past
+  // k ~ 3000 no cluster shape fits and the grid-wide engine runs instead
+  return use_grid_engine() || !cluster_engine_fits(static_cast<int>(I->k))
+             ? run_engine(I, A, a_begin, a_end)
+             : run_cluster_engine(I, A, a_begin, a_end, keys16);
 }
 
 EngineCtl g_last_ctl;  // instrumentation of the last engine run

@@ -212,3 +212,20 @@ def test_medium_solves_lists_rescans_and_key_paths(dev, oracle, tile, monkeypatc
             opts = SolverOptions(refine_to_fixpoint=bool(it % 2))
             assert same_report(dev.solve(inst, solver, opts), oracle.solve(inst, solver, opts)), \
                 (it, solver, n, k, max_cost)
+
+
+def test_grid_engine_matches_oracle(dev, oracle, monkeypatch):
+    """The grid-wide cooperative engine: what solves run on when k is too
+    large for the one-cluster engine's shared memory (k ~ 3000 and up).
+    Forced here on small instances, bit-exact against the oracle."""
+    monkeypatch.setenv("LBDD_B200_ENGINE", "grid")
+    rng = po.Mt19937_64(4242)
+    for it in range(4):
+        n, k = 200 + rng() % 400, 10 + rng() % 60
+        max_cost = [100, 5000][it % 2]
+        inst = po.random_instance(rng, n=n, k=k, max_cost=max_cost, penalty_hi=max_cost // 2 + 1,
+                                  total_capacity=int(n * [0.8, 1.0][it % 2]))
+        for solver in ["asral", "strict"]:
+            opts = SolverOptions(refine_to_fixpoint=bool(it % 2))
+            assert same_report(dev.solve(inst, solver, opts), oracle.solve(inst, solver, opts)), \
+                (it, solver, n, k, max_cost)

@@ -20,7 +20,7 @@
 
 // threads per CTA of the cluster engine (cluster.cu)
 #ifndef LBDD_CLUSTER_THREADS
-#define LBDD_CLUSTER_THREADS 512
+#define LBDD_CLUSTER_THREADS 384
 #endif
 
 #include <cstdint>

@@ -140,19 +140,19 @@ lbdd_status lbdd_b200_instance_create_device(const lbdd_instance_desc* desc,
                                              int64_t pitch_elems, int device,
                                              lbdd_b200_instance** out);
 
-/* Synthetic generator, device-side: euclidean costs
- * (llround(1000*dist), clamped to >= 1, instgen.hpp:87-90) for n demand
- * points and k center points drawn from a counter-based RNG, total capacity
- * round(theta*n) spread over centers (capacity_skew 0: uniform multinomial
- * as instgen.hpp:267-271; > 0: Zipf-like skew), penalties drawn from
- * [pen_lo, pen_hi] (mixed_families != 0 mixes constant/linear/table).
- * Not byte-identical to the reference's mt19937_64 stream — that one is a
- * sequential CPU generator; use lbdd_b200_instance_create with its output
- * for parity runs. */
-lbdd_status lbdd_b200_instance_generate(int64_t n, int64_t k, double theta,
-                                        int64_t pen_lo, int64_t pen_hi,
-                                        int32_t mixed_families,
-                                        double capacity_skew, uint64_t seed,
+/* Synthetic generator, device-side, spec "lbdd-synth-v2" (bit-identical to
+ * the host generator synth_instances.py): integer grid points from a
+ * counter-based splitmix64 stream, euclidean costs
+ * max(1, floor(sqrt(dx^2+dy^2)/10 + 0.5)) in [1, 1414]; total capacity
+ * n*theta_num/theta_den over integer weights 1 + h % cap_spread
+ * (heterogeneous); penalties from [pen_lo, pen_hi] (mixed_families != 0
+ * mixes constant / linear / table, core.hpp:43-96). Not the reference's
+ * mt19937_64 stream (instgen.hpp:245) — that one is a sequential CPU
+ * generator; use lbdd_b200_instance_create with its output instead. */
+lbdd_status lbdd_b200_instance_generate(int64_t n, int64_t k, int64_t theta_num,
+                                        int64_t theta_den, int64_t pen_lo,
+                                        int64_t pen_hi, int32_t mixed_families,
+                                        int64_t cap_spread, uint64_t seed,
                                         int device, lbdd_b200_instance** out);
 
 lbdd_status lbdd_b200_instance_destroy(lbdd_b200_instance* inst);

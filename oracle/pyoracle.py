@@ -175,6 +175,11 @@ class CLib:
                                              C.byref(ns), C.byref(done), C.byref(setup)))
         return ns.value, done.value, setup.value
 
+    def instance(self, inst) -> "RefInstance":
+        """Reference-only: the instance converted once (int64 CostMatrix) for
+        repeated bounded samples (lbdd_ref_asral_sample_inst)."""
+        return RefInstance(self, inst)
+
     def oracle_solve(self, inst, strict, size_limit=2000):
         """Reference-only: exact min-cost-flow optimum (oracle.hpp:144)."""
         h = DescHolder(inst)
@@ -190,6 +195,34 @@ class CLib:
 
 _ORACLE = None
 _REF = None
+
+
+class RefInstance:
+    """A reference lbdd::ProblemInstance held by oracle/_ref (bench.py's
+    reference arm and cpu_baseline leg)."""
+
+    def __init__(self, lib: CLib, inst: ProblemInstance):
+        self.lib = lib
+        self.n = inst.n
+        new = lib._fn("instance_new")
+        new.restype = C.c_void_p
+        holder = DescHolder(inst)  # keeps the numpy buffers alive across the call
+        self.h = new(holder.ref)
+        if not self.h:
+            raise RuntimeError(lib._err().decode())
+
+    def sample(self, max_arrivals: int):
+        """(elapsed ns incl. setup, arrivals done, setup ns)."""
+        ns, done, setup = C.c_int64(), C.c_int64(), C.c_int64()
+        self.lib._check(self.lib._fn("asral_sample_inst")(C.c_void_p(self.h),
+                                                          C.c_int64(max_arrivals), C.byref(ns),
+                                                          C.byref(done), C.byref(setup)))
+        return ns.value, done.value, setup.value
+
+    def close(self):
+        if self.h:
+            self.lib._fn("instance_free")(C.c_void_p(self.h))
+            self.h = None
 
 
 def oracle() -> CLib:

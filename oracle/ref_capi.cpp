@@ -7,7 +7,9 @@
 // entry point constructs the reference's own types and calls its functions,
 // so the outputs are the reference's outputs. Used by tests/ (parity and
 // golden-vector generation) and by bench.py's reference / cpu_baseline arm.
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -381,6 +383,207 @@ int lbdd_ref_asral_sample(const lbdd_instance_desc* desc, int64_t max_arrivals,
       } else {
         st.delta = lbdd::checked_add(
             st.delta, lbdd::checked_add(cost, lbdd::refund_penalty(center, load)));
+        lbdd::negative_path_refine(st, s);
+      }
+      ++done;
+    }
+    *elapsed_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now() - start).count();
+    *arrivals_done = done;
+  });
+}
+}  // extern "C"
+
+extern "C" {
+// The reference's asral_solve (solver.hpp:133-170) run to completion, with
+// progress marks: the loop of solver.hpp:143-166 over the reference's own
+// types and functions, closed by the reference's own detail::finish_report
+// (objective recount + tracked-delta check). marks[i] = elapsed ns after
+// (i + 1) * mark_every arrivals; a line goes to stderr at each mark. Used to
+// pin the GPU solve at scale (tests/golden/scale/) and to time the full CPU
+// solve for bench.py's baseline. Sequential (the reference's
+// worker pool can lose a wake-up).
+// ckpt_every > 0: every ckpt_every arrivals, the centers of the arrivals so
+// far (in arrival order, int16) are written to <ckpt_prefix><count>.i16 —
+// resumable states for the bench's steady-state CPU samples
+// (lbdd_ref_resume_new).
+int lbdd_ref_asral_run(const lbdd_instance_desc* desc, int64_t mark_every,
+                       int64_t* marks, int64_t max_marks, lbdd_solve_report* report,
+                       int32_t* assignment, int64_t* load, int64_t* setup_ns,
+                       int64_t ckpt_every, const char* ckpt_prefix) {
+  return guarded([&] {
+    auto inst = to_instance(desc);
+    lbdd::require_valid_instance(inst);
+    const auto start = std::chrono::steady_clock::now();
+    auto since = [&] {
+      return std::chrono::duration_cast<std::chrono::nanoseconds>(
+                 std::chrono::steady_clock::now() - start).count();
+    };
+    lbdd::SolverState st(inst);
+    auto queue = lbdd::detail::build_arrival_queue(inst);
+    *setup_ns = since();
+    int64_t done = 0;
+    std::vector<lbdd::DemandId> popped;
+    while (!queue.empty()) {
+      const auto [cost, d, s] = queue.top();
+      queue.pop();
+      if (ckpt_every > 0) popped.push_back(d);
+      st.index.insert(d, s);
+      st.allotment.assign(d, s);
+      lbdd::negative_cycle_refine(st, s);
+      const auto& center = inst.centers[static_cast<std::size_t>(s)];
+      const lbdd::Count ld = st.allotment.load[static_cast<std::size_t>(s)];
+      if (ld <= center.capacity) {
+        st.delta = lbdd::checked_add(st.delta, cost);
+      } else {
+        st.delta = lbdd::checked_add(
+            st.delta, lbdd::checked_add(cost, lbdd::refund_penalty(center, ld)));
+        lbdd::negative_path_refine(st, s);
+      }
+      ++done;
+      if (mark_every > 0 && done % mark_every == 0) {
+        const int64_t i = done / mark_every - 1;
+        const int64_t t = since();
+        if (i < max_marks) marks[i] = t;
+        std::fprintf(stderr, "[ref] %lld arrivals %.1f s delta %lld\n",
+                     static_cast<long long>(done), t / 1e9,
+                     static_cast<long long>(st.delta));
+        std::fflush(stderr);
+      }
+      if (ckpt_every > 0 && done % ckpt_every == 0) {
+        std::vector<int16_t> cs(popped.size());
+        for (std::size_t i = 0; i < popped.size(); ++i) {
+          cs[i] = static_cast<int16_t>(st.allotment.assignment[static_cast<std::size_t>(popped[i])]);
+        }
+        const std::string path = std::string(ckpt_prefix) + std::to_string(done) + ".i16";
+        if (FILE* f = std::fopen(path.c_str(), "wb")) {
+          std::fwrite(cs.data(), sizeof(int16_t), cs.size(), f);
+          std::fclose(f);
+        }
+      }
+    }
+    const auto r = lbdd::detail::finish_report(st, "asral", start);
+    fill_report(r, LBDD_SOLVER_ASRAL, report, assignment, load);
+  });
+}
+}  // extern "C"
+
+extern "C" {
+// A reference ProblemInstance (int64 CostMatrix, core.hpp:105-143) built once,
+// so repeated bounded samples of the same instance do not pay the conversion.
+void* lbdd_ref_instance_new(const lbdd_instance_desc* desc) {
+  try {
+    return new lbdd::ProblemInstance(to_instance(desc));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void lbdd_ref_instance_free(void* inst) { delete static_cast<lbdd::ProblemInstance*>(inst); }
+
+// lbdd_ref_asral_sample on a prebuilt instance: setup = require_valid_instance
+// + empty SolverState + build_arrival_queue (solver.hpp:135-141), then the
+// first max_arrivals iterations of solver.hpp:143-166.
+int lbdd_ref_asral_sample_inst(const void* handle, int64_t max_arrivals, int64_t* elapsed_ns,
+                               int64_t* arrivals_done, int64_t* setup_ns) {
+  return guarded([&] {
+    const auto& inst = *static_cast<const lbdd::ProblemInstance*>(handle);
+    const auto start = std::chrono::steady_clock::now();
+    lbdd::require_valid_instance(inst);
+    lbdd::SolverState st(inst);
+    auto queue = lbdd::detail::build_arrival_queue(inst);
+    *setup_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                    std::chrono::steady_clock::now() - start).count();
+    int64_t done = 0;
+    while (!queue.empty() && done < max_arrivals) {
+      const auto [cost, d, s] = queue.top();
+      queue.pop();
+      st.index.insert(d, s);
+      st.allotment.assign(d, s);
+      lbdd::negative_cycle_refine(st, s);
+      const auto& center = inst.centers[static_cast<std::size_t>(s)];
+      const lbdd::Count ld = st.allotment.load[static_cast<std::size_t>(s)];
+      if (ld <= center.capacity) {
+        st.delta = lbdd::checked_add(st.delta, cost);
+      } else {
+        st.delta = lbdd::checked_add(
+            st.delta, lbdd::checked_add(cost, lbdd::refund_penalty(center, ld)));
+        lbdd::negative_path_refine(st, s);
+      }
+      ++done;
+    }
+    *elapsed_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now() - start).count();
+    *arrivals_done = done;
+  });
+}
+}  // extern "C"
+
+namespace {
+// A reference solver state resumed mid-solve: the arrival queue of
+// solver.hpp:141 with its first X entries popped, and
+// SolverState::from_allotment (solver.hpp:57-66, the reference's own
+// constructor over a preexisting allotment) on the allotment the reference
+// itself reached after those X arrivals (its checkpoint file).
+struct Resumed {
+  const lbdd::ProblemInstance* inst;
+  lbdd::SolverState st;
+  lbdd::detail::ArrivalQueue queue;
+  Resumed(const lbdd::ProblemInstance& i, lbdd::SolverState&& s, lbdd::detail::ArrivalQueue&& q)
+      : inst(&i), st(std::move(s)), queue(std::move(q)) {}
+};
+}  // namespace
+
+extern "C" {
+void* lbdd_ref_resume_new(const void* handle, const int16_t* centers, int64_t count,
+                          int64_t* setup_ns) {
+  try {
+    const auto& inst = *static_cast<const lbdd::ProblemInstance*>(handle);
+    const auto start = std::chrono::steady_clock::now();
+    auto queue = lbdd::detail::build_arrival_queue(inst);
+    auto allot = lbdd::Allotment::empty(inst.n(), inst.k());
+    for (int64_t i = 0; i < count; ++i) {
+      const auto [cost, d, s] = queue.top();
+      queue.pop();
+      allot.assign(d, centers[i]);
+    }
+    auto st = lbdd::SolverState::from_allotment(inst, allot);
+    auto* r = new Resumed(inst, std::move(st), std::move(queue));
+    *setup_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                    std::chrono::steady_clock::now() - start).count();
+    return r;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void lbdd_ref_resume_free(void* r) { delete static_cast<Resumed*>(r); }
+
+// The next max_arrivals iterations of solver.hpp:143-166 from the resumed
+// state (the state advances: consecutive calls time consecutive arrivals).
+int lbdd_ref_resume_step(void* handle, int64_t max_arrivals, int64_t* elapsed_ns,
+                         int64_t* arrivals_done) {
+  return guarded([&] {
+    auto& r = *static_cast<Resumed*>(handle);
+    auto& st = r.st;
+    const auto& inst = *r.inst;
+    const auto start = std::chrono::steady_clock::now();
+    int64_t done = 0;
+    while (!r.queue.empty() && done < max_arrivals) {
+      const auto [cost, d, s] = r.queue.top();
+      r.queue.pop();
+      st.index.insert(d, s);
+      st.allotment.assign(d, s);
+      lbdd::negative_cycle_refine(st, s);
+      const auto& center = inst.centers[static_cast<std::size_t>(s)];
+      const lbdd::Count ld = st.allotment.load[static_cast<std::size_t>(s)];
+      if (ld <= center.capacity) {
+        st.delta = lbdd::checked_add(st.delta, cost);
+      } else {
+        st.delta = lbdd::checked_add(
+            st.delta, lbdd::checked_add(cost, lbdd::refund_penalty(center, ld)));
         lbdd::negative_path_refine(st, s);
       }
       ++done;

@@ -931,6 +931,17 @@ void solve_strict(lbdd_b200_instance* I0, const lbdd_solver_options* o,
   A.dummies = W->dummies.p;
   A.check_invariants = o && o->check_invariants;
   if (o && o->strict_order && o->strict_order_len > 0) {
+    // The kernel indexes the cost matrix and home[] with these ids: reject
+    // out-of-range ids (std::vector UB in the reference) and report a
+    // repeated demand the way the reference's SubspaceIndex::insert does
+    // (subspace.hpp:46-49, std::logic_error).
+    std::vector<uint8_t> seen(static_cast<size_t>(n), 0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t d = o->strict_order[i];
+      if (d < 0 || d >= n) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: strict order entry out of range");
+      if (seen[static_cast<size_t>(d)]) raise(LBDD_ERR_LOGIC, "lbdd: demand already indexed");
+      seen[static_cast<size_t>(d)] = 1;
+    }
     W->order.ensure(n);
     CUDA_OK(cudaMemcpyAsync(W->order.p, o->strict_order, sizeof(int32_t) * n,
                             cudaMemcpyHostToDevice, W->stream));
@@ -939,6 +950,10 @@ void solve_strict(lbdd_b200_instance* I0, const lbdd_solver_options* o,
   // augmented instance: the overflow column max+1 widens the range by one
   const bool keys16 = keys_fit_int16(I0) && I0->max_cost + 2 - I0->min_cost <= 32000;
   const EngineCtl ctl = run_solver_engine(W, A, 0, n, keys16);
+  if (W != I0) {  // the engine ran on the augmented instance: report its time
+    I0->engine_ns += W->engine_ns;
+    I0->engine_launches += W->engine_launches;
+  }
   // capacity / placeholder accounting (solver.hpp:279-289)
   std::vector<int64_t> dummies(k);
   CUDA_OK(cudaMemcpyAsync(dummies.data(), W->dummies.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost,
@@ -1110,71 +1125,66 @@ lbdd_status lbdd_b200_instance_create_device(const lbdd_instance_desc* desc, con
   });
 }
 
-lbdd_status lbdd_b200_instance_generate(int64_t n, int64_t k, double theta, int64_t pen_lo,
-                                        int64_t pen_hi, int32_t mixed_families,
-                                        double capacity_skew, uint64_t seed, int device,
-                                        lbdd_b200_instance** out) {
+lbdd_status lbdd_b200_instance_generate(int64_t n, int64_t k, int64_t theta_num,
+                                        int64_t theta_den, int64_t pen_lo, int64_t pen_hi,
+                                        int32_t mixed_families, int64_t cap_spread,
+                                        uint64_t seed, int device, lbdd_b200_instance** out) {
   return guarded([&] {
     if (n < 1 || k < 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: n and k must be >= 1");
-    if (theta <= 0.0) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: theta must be positive");
+    if (theta_num < 1 || theta_den < 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: theta must be positive");
     if (pen_lo < 1 || pen_hi < pen_lo) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: bad penalty range");
+    if (cap_spread < 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: cap_spread must be >= 1");
     std::unique_ptr<lbdd_b200_instance> I(new_instance(device, n, k));
     CUDA_OK(cudaMalloc(&I->d_cm, sizeof(int32_t) * n * I->pitch));
     I->owns_cm = true;
-    // host RNG for the k centers (splitmix64 stream)
-    uint64_t st = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
-    auto next = [&st]() {
-      uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+    // spec "lbdd-synth-v2" (synth_instances.py): stream(seed, t, i) =
+    // mix(mix(seed ^ t) + (i + 1) * golden)
+    auto mix = [](uint64_t z) {
       z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
       return z ^ (z >> 31);
     };
-    auto u01 = [&]() { return static_cast<double>(next() >> 11) * 0x1.0p-53; };
-    auto below = [&](uint64_t b) { return next() % b; };
-    std::vector<double2> centers(k);
-    for (auto& c : centers) c = make_double2(u01(), u01());
-    DevBuf<double2> dc;
-    dc.ensure(k);
-    CUDA_OK(cudaMemcpyAsync(dc.p, centers.data(), sizeof(double2) * k, cudaMemcpyHostToDevice, I->stream));
+    auto stream = [&](uint64_t tag, uint64_t i) {
+      return mix(mix(seed ^ tag) + (i + 1) * 0x9E3779B97F4A7C15ull);
+    };
+    const ulonglong4 base = make_ulonglong4(mix(seed ^ 1), mix(seed ^ 2), mix(seed ^ 3), mix(seed ^ 4));
     g_launches++;
     generate_costs_kernel<<<I->num_sms * 8, 256, 0, I->stream>>>(I->d_cm, I->pitch, 0, n,
-                                                                static_cast<int32_t>(k), seed, dc.p);
+                                                                static_cast<int32_t>(k), base);
     CUDA_OK(cudaGetLastError());
-    // capacities: total round(theta*n), multinomial over centers with
-    // weight (s+1)^-skew (skew 0: uniform, instgen.hpp:267-271)
-    const int64_t total = static_cast<int64_t>(std::llround(theta * static_cast<double>(n)));
-    std::vector<double> w(k);
-    double wsum = 0;
+    // capacities: total = n * theta_num // theta_den over integer weights
+    // 1 + stream(5, s) % cap_spread; the remainder adds 1 to centers 0, 1, ...
+    const int64_t total = n * theta_num / theta_den;
+    std::vector<int64_t> w(k), cap(k);
+    int64_t wsum = 0, assigned = 0;
     for (int64_t s = 0; s < k; ++s) {
-      w[s] = capacity_skew > 0 ? std::pow(static_cast<double>(s + 1), -capacity_skew) : 1.0;
+      w[s] = 1 + static_cast<int64_t>(stream(5, s) % static_cast<uint64_t>(cap_spread));
       wsum += w[s];
     }
-    std::vector<int64_t> cap(k, 0);
-    int64_t assigned = 0;
     for (int64_t s = 0; s < k; ++s) {
-      cap[s] = static_cast<int64_t>(std::floor(static_cast<double>(total) * w[s] / wsum));
+      cap[s] = static_cast<int64_t>(static_cast<__int128>(total) * w[s] / wsum);
       assigned += cap[s];
     }
-    for (int64_t r = assigned; r < total; ++r) cap[below(k)]++;
-    if (capacity_skew > 0) {  // skewed capacities land on random centers
-      for (int64_t s = k - 1; s > 0; --s) std::swap(cap[s], cap[below(s + 1)]);
-    }
+    for (int64_t s = 0; s < total - assigned; ++s) cap[s]++;
     std::vector<int32_t> fam(k);
     std::vector<int64_t> off(k + 1, 0), par;
+    const uint64_t span = static_cast<uint64_t>(pen_hi - pen_lo + 1);
     for (int64_t s = 0; s < k; ++s) {
-      const int64_t base = pen_lo + static_cast<int64_t>(below(pen_hi - pen_lo + 1));
-      const int f = mixed_families ? static_cast<int>(below(3)) : 0;
+      const uint64_t p = stream(6, s);
+      const int f = mixed_families ? static_cast<int>(p % 3) : 0;
+      const int64_t base_pen = pen_lo + static_cast<int64_t>((p >> 8) % span);
       fam[s] = f;
       if (f == 0) {
-        par.push_back(base);
+        par.push_back(base_pen);
       } else if (f == 1) {
-        par.push_back(base);
-        par.push_back(static_cast<int64_t>(below(6)));
+        par.push_back(base_pen);
+        par.push_back(static_cast<int64_t>((p >> 24) % 6));
       } else {
-        int64_t v = base;
-        for (int t = 0; t < 4; ++t) {
+        int64_t v = base_pen;
+        par.push_back(v);
+        for (int t = 1; t < 4; ++t) {
+          v += static_cast<int64_t>((p >> (32 + 3 * t)) % 8);
           par.push_back(v);
-          v += static_cast<int64_t>(below(8));
         }
       }
       off[s + 1] = static_cast<int64_t>(par.size());
@@ -1182,7 +1192,6 @@ lbdd_status lbdd_b200_instance_generate(int64_t n, int64_t k, double theta, int6
     lbdd_instance_desc d{n, k, nullptr, cap.data(), fam.data(), off.data(), par.data()};
     upload_centers(I.get(), &d);
     CUDA_OK(cudaStreamSynchronize(I->stream));
-    dc.release();
     *out = I.release();
   });
 }

@@ -220,40 +220,43 @@ __global__ void objective_kernel(const int32_t* __restrict__ cm, int64_t pitch, 
 }
 
 namespace {
-__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
-  x += 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
-__device__ __forceinline__ double u01(uint64_t x) {
-  return static_cast<double>(splitmix64(x) >> 11) * 0x1.0p-53;
+// splitmix64 finaliser; synth_instances.py mix()
+__device__ __forceinline__ uint64_t synth_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
 }
 }  // namespace
 
-// Synthetic euclidean costs: llround(1000 * |demand - center|), >= 1
-// (scaled_cost, instgen.hpp:87-90). Points from a counter-based RNG so any
-// row range can be generated independently (sharded generation).
+// Synthetic euclidean costs, spec "lbdd-synth-v2" (synth_instances.py, bit
+// for bit): integer points on a 10000 x 10000 grid from a counter-based
+// stream, cost = max(1, floor(sqrt(dx^2 + dy^2) / 10 + 0.5)). The double
+// sqrt and division are IEEE correctly rounded here and in numpy, so the
+// host generator and this kernel agree exactly. Any row range can be
+// generated independently (sharded generation). base[t] = mix(seed ^ t).
 __global__ void generate_costs_kernel(int32_t* __restrict__ cm, int64_t pitch, int64_t row0,
-                                      int64_t rows, int32_t k, uint64_t seed,
-                                      const double2* __restrict__ centers) {
+                                      int64_t rows, int32_t k, ulonglong4 base) {
   const int nv = static_cast<int>(pitch >> 2);
   const int64_t total = rows * nv;
+  constexpr uint64_t kGold = 0x9E3779B97F4A7C15ull;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = i / nv;
     const int v = static_cast<int>(i - r * nv);
-    const int64_t d = row0 + r;
-    const double dx = u01(seed ^ (0x5bd1e995ull * (2 * d + 1)));
-    const double dy = u01(seed ^ (0x5bd1e995ull * (2 * d + 2)) ^ 0xabcdefull);
+    const uint64_t d1 = static_cast<uint64_t>(row0 + r) + 1;
+    const int64_t dx = static_cast<int64_t>(synth_mix(base.x + d1 * kGold) % 10000ull);
+    const int64_t dy = static_cast<int64_t>(synth_mix(base.y + d1 * kGold) % 10000ull);
     int32_t out[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int j = v * 4 + c;
       if (j < k) {
-        const double2 cp = centers[j];
-        long long q = llround(hypot(dx - cp.x, dy - cp.y) * 1000.0);
-        out[c] = static_cast<int32_t>(q < 1 ? 1 : q);
+        const uint64_t j1 = static_cast<uint64_t>(j) + 1;
+        const int64_t ex = dx - static_cast<int64_t>(synth_mix(base.z + j1 * kGold) % 10000ull);
+        const int64_t ey = dy - static_cast<int64_t>(synth_mix(base.w + j1 * kGold) % 10000ull);
+        const double q = static_cast<double>(ex * ex + ey * ey);
+        const double c2 = floor(__dadd_rn(__ddiv_rn(__dsqrt_rn(q), 10.0), 0.5));
+        out[c] = c2 < 1.0 ? 1 : static_cast<int32_t>(c2);
       } else {
         out[c] = INT32_MAX;  // row padding, never read as a cost
       }

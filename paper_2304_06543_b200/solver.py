@@ -38,9 +38,9 @@ _lib.lbdd_b200_engine_counters.argtypes = [_abi.I64P]
 _lib.lbdd_b200_instance_create.argtypes = [C.POINTER(_abi.InstanceDesc), C.c_int, C.POINTER(_P)]
 _lib.lbdd_b200_instance_create_device.argtypes = [C.POINTER(_abi.InstanceDesc), _P, C.c_int64,
                                                   C.c_int, C.POINTER(_P)]
-_lib.lbdd_b200_instance_generate.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_int64,
-                                             C.c_int64, C.c_int32, C.c_double, C.c_uint64,
-                                             C.c_int, C.POINTER(_P)]
+_lib.lbdd_b200_instance_generate.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                             C.c_int64, C.c_int64, C.c_int32, C.c_int64,
+                                             C.c_uint64, C.c_int, C.POINTER(_P)]
 _lib.lbdd_b200_instance_destroy.argtypes = [_P]
 _lib.lbdd_b200_instance_shape.argtypes = [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
 _lib.lbdd_b200_instance_centers.argtypes = [_P, _abi.I64P, _abi.I32P, _abi.I64P, _abi.I64P,
@@ -138,13 +138,23 @@ class DeviceInstance:
         return DeviceInstance(out.value, keep=keep)
 
     @staticmethod
-    def generate(n: int, k: int, theta: float = 0.8, pen_lo: int = 1, pen_hi: int = 200,
-                 mixed_families: bool = False, capacity_skew: float = 0.0, seed: int = 1,
+    def generate(n: int, k: int, seed: int = 20250, theta_num: int = 8, theta_den: int = 10,
+                 pen_lo: int = 1, pen_hi: int = 200, mixed: bool = True, cap_spread: int = 16,
                  device: int = 0) -> "DeviceInstance":
+        """Generate in HBM the synth_instances.SynthSpec instance with these
+        fields (spec lbdd-synth-v2, bit-identical to the host generator)."""
         out = C.c_void_p()
-        _check(_lib.lbdd_b200_instance_generate(n, k, theta, pen_lo, pen_hi, int(mixed_families),
-                                                capacity_skew, seed, device, C.byref(out)))
+        _check(_lib.lbdd_b200_instance_generate(n, k, theta_num, theta_den, pen_lo, pen_hi,
+                                                int(mixed), cap_spread, seed, device,
+                                                C.byref(out)))
         return DeviceInstance(out.value)
+
+    @staticmethod
+    def from_spec(spec, device: int = 0) -> "DeviceInstance":
+        """DeviceInstance.generate from a synth_instances.SynthSpec."""
+        return DeviceInstance.generate(spec.n, spec.k, spec.seed, spec.theta_num, spec.theta_den,
+                                       spec.pen_lo, spec.pen_hi, spec.mixed, spec.cap_spread,
+                                       device)
 
     def centers(self):
         npar = C.c_int64()

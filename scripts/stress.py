@@ -18,8 +18,9 @@ while time.time() < t_end:
     n, k = shapes[it % len(shapes)]
     seed = 1000 + it
     theta = [0.8, 1.0, 0.6, 1.2][it % 4]
-    dev = S.DeviceInstance.generate(n, k, theta=theta, pen_lo=1, pen_hi=200, mixed_families=True,
-                                    capacity_skew=[0.5, 0.0, 1.0][it % 3], seed=seed, device=0)
+    tn, td = {0.8: (8, 10), 1.0: (1, 1), 0.6: (6, 10), 1.2: (12, 10)}[theta]
+    dev = S.DeviceInstance.generate(n, k, seed=seed, theta_num=tn, theta_den=td,
+                                    cap_spread=[16, 1, 64][it % 3])
     host = dev.costs(); cap, fam, off, par = dev.centers()
     params = [list(par[off[i]:off[i + 1]]) for i in range(k)]
     inst = ProblemInstance.from_arrays(host, cap, fam, params)

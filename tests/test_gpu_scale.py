@@ -3,6 +3,8 @@ run these sizes in seconds)."""
 import numpy as np
 import pytest
 
+import synth_instances as SI
+
 import pyoracle as po
 
 pytestmark = pytest.mark.gpu
@@ -11,8 +13,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def big(dev):
     # configs[1] shape: |D| = 1M x |S| = 1000 int32, heterogeneous capacities
-    inst = dev.DeviceInstance.generate(1_000_000, 1000, theta=0.8, mixed_families=True,
-                                       capacity_skew=0.5, seed=11)
+    inst = dev.DeviceInstance.generate(1_000_000, 1000, seed=11)
     yield inst
     inst.close()
 
@@ -52,10 +53,22 @@ def test_greedy_full_size_recount(dev, big):
 
 
 def test_asral_medium_properties(dev):
-    inst = dev.DeviceInstance.generate(20_000, 500, theta=0.7, mixed_families=True, seed=5)
+    inst = dev.DeviceInstance.generate(20_000, 500, seed=5, theta_num=7, theta_den=10)
     a = dev.asral_solve(inst)          # the engine recounts the objective itself
     g = dev.greedy_solve(inst)
     assert a.objective <= g.objective  # acceptance.cpp:182 dominance
     assert np.bincount(a.assignment, minlength=inst.k).tolist() == a.load.tolist()
     assert not dev.gamma_has_negative_cycle(inst, a.assignment)  # Lemma invariant
     assert dev.evaluate_objective(inst, a.assignment) == a.objective
+
+
+def test_device_generator_matches_host_spec(dev, big):
+    """lbdd_b200_instance_generate == synth_instances.py (spec lbdd-synth-v2)
+    bit for bit: sampled row blocks and the center arrays."""
+    spec = SI.SynthSpec(1_000_000, 1000, seed=11)
+    for r0 in (0, 123_457, 999_000):
+        assert np.array_equal(big.costs(r0, 1000), SI.cost_rows(spec, r0, 1000))
+    cap, fam, off, par = big.centers()
+    hc, hf, ho, hp = SI.centers(spec)
+    assert np.array_equal(cap, hc) and np.array_equal(fam, hf)
+    assert np.array_equal(off, ho) and np.array_equal(par[:len(hp)], hp)

@@ -133,7 +133,7 @@ struct lbdd_b200_instance {
   DevBuf<int32_t> P[2][2];
   DevBuf<int64_t> D[2][2], B[2][3];
   DevBuf<int64_t> load, dummies, M, colW, single_gain, pi;
-  DevBuf<int32_t> dirty, log_d, log_to, log_n;
+  DevBuf<int32_t> dirty, log_d, log_to, log_n, add_ids, add_cnt;
   DevBuf<int64_t> MX;
   DevBuf<uint8_t> LN;
   int cluster_size = 0;  // chosen once per instance
@@ -170,6 +170,7 @@ struct lbdd_b200_instance {
     }
     single_out.release(); rowver.release(); load.release(); dummies.release(); M.release();
     pi.release(); dirty.release(); log_d.release(); log_to.release(); log_n.release();
+    add_ids.release(); add_cnt.release();
     MX.release(); LN.release();
     colW.release();
     single_gain.release(); ctl.release(); bar.release(); path.release(); dumflag.release();
@@ -669,7 +670,8 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
 size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
   return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * s + 2 * sizeof(cl::Pub) + 8 * 16 +
          2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) + 8 * (k + 1) +
-         4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * static_cast<size_t>(cl::kMaxCS) * s + 4 * 2 * cl::kMaxSeg +
+         4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * static_cast<size_t>(cl::kMaxCS) * s + 4 * 3 * cl::kMaxSeg +
+         4 * 2 * cl::kMaxMine + 4 * (2 * cl::kMaxSeg + 2) +
          8 * 16 + 8 * 16 +
          sizeof(PathEdge) * (k + 1) + 12 * block + 4 * 16 +
          4 * static_cast<size_t>(cl::kRowSlots) * ((k + 31) / 32) +
@@ -765,6 +767,14 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
   A.log_to = I->log_to.p;
   A.log_n = I->log_n.p;
   A.log_cap = kLogCap;
+  // per-center add lists: the T3 rescan candidates of a center are its
+  // launch-start bucket plus the demands that moved to it since
+  constexpr int32_t kAddCap = 128;
+  I->add_ids.ensure(static_cast<size_t>(k) * kAddCap);
+  I->add_cnt.ensure(k);
+  A.add_ids = I->add_ids.p;
+  A.add_cnt = I->add_cnt.p;
+  A.add_cap = kAddCap;
   int64_t a = a_begin;
   int64_t* pi = I->pi.p;
   int32_t* dirty = I->dirty.p;
@@ -775,6 +785,7 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
     A.bk_off = I->ib_off.p;
     A.bk_ids = I->ib_sorted.p;
     CUDA_OK(cudaMemsetAsync(I->log_n.p, 0, sizeof(int32_t), I->stream));
+    CUDA_OK(cudaMemsetAsync(I->add_cnt.p, 0, sizeof(int32_t) * k, I->stream));
     g_launches++;
     ensure_kernel_events(I);
     CUDA_OK(cudaEventRecord(I->kev[0], I->stream));

@@ -48,6 +48,7 @@ constexpr int kStage = 256;            // frontier entries staged per pass
 constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
 constexpr int kMaxSeg = 32;            // source rows rescanned per apply via the index
 constexpr int kRowSlots = 8;           // source rows of a row-mode rescan (column bitmaps)
+constexpr int kMaxMine = 1024;         // invalidated (segment, column) pairs a CTA owns per rescan
 
 // A frontier entry as pushed into every CTA's inbox: the node (bit 31: a
 // surplus placeholder sits there, strict-mode edge rule) and its label with
@@ -110,7 +111,11 @@ struct CS {           // shared-memory layout of one CTA
   int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
   int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
   FEntry* cmp;        // [kMaxCS * s] the pushed entries, compacted by the exchange
-  int32_t* seg;       // [2 * kMaxSeg] rescan segments (slot, prefix end)
+  int32_t* seg;       // [3 * kMaxSeg] rescan segments (slot, prefix end, bucket count)
+  int32_t* mine;      // [kMaxMine] my invalidated columns of a rescan ((g << 16) | j, then j by segment)
+  int32_t* mine2;     // [kMaxMine] scratch of the counting sort
+  int32_t* segmine;   // [kMaxSeg + 1] my columns per segment, then their offsets
+  int32_t* segcur;    // [kMaxSeg] counting-sort cursors
   int64_t* dbg;       // [16] instrumentation counters
   int64_t* prof;      // [16] lead-thread cycle counters per phase
   int16_t* wt;        // [k * s] transfer keys of every row into my columns
@@ -132,7 +137,11 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
 
   S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
   S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
-  S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 2 * kMaxSeg;
+  S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 3 * kMaxSeg;
+  S.mine = reinterpret_cast<int32_t*>(p); p += 4 * kMaxMine;
+  S.mine2 = reinterpret_cast<int32_t*>(p); p += 4 * kMaxMine;
+  S.segmine = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxSeg + 2);  // even: keeps 8 B alignment
+  S.segcur = reinterpret_cast<int32_t*>(p); p += 4 * kMaxSeg;
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
@@ -398,6 +407,11 @@ __device__ __forceinline__ void log_move(const EngineArgs& A, int32_t d, int32_t
     A.log_to[i] = to;
   }
   *A.log_n = i + 1;  // past the cap: overflowed, rescans scan every demand
+  if (A.add_cnt != nullptr) {  // the per-center add list of `to`
+    const int32_t c = A.add_cnt[to];
+    if (c < A.add_cap) A.add_ids[static_cast<int64_t>(to) * A.add_cap + c] = d;
+    A.add_cnt[to] = c + 1;  // past add_cap: rescans of `to` use the move log
+  }
 }
 
 __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
@@ -952,69 +966,126 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   PROF_MARK(X, 12);  // apply exchanges
   // ---- T3: rescans of the invalidated entries over the final buckets ----
   // Members of a source center u: its segment of the bucket index built at
-  // launch start (A.bk_ids[A.bk_off[u] ..)), plus demands that moved to u
-  // since (the move log) — each still checked against home[]. A log that
-  // overflowed falls back to scanning every demand.
+  // launch start (A.bk_ids[A.bk_off[u] ..)), then its add list (demands that
+  // moved to u since) — each still checked against home[]. An overflowed
+  // add list falls back to the whole move log, an overflowed log to every
+  // demand. Work split: every CTA walks all candidates and rebuilds only the
+  // entries of ITS columns (the owner is the only writer of its lists in
+  // this phase), so the member-row reads spread over the whole cluster.
   int total = 0;
   for (int i = 0; i < len; ++i) total += (S.path[i].kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
   if (total > 0) {
-    int32_t* seg = S.seg;  // [2 * kMaxSeg]: (slot, prefix end)
+    int32_t* seg = S.seg;  // [3 * kMaxSeg]: (slot, prefix end, bucket count)
     int nseg = 0;
     int64_t nbase = 0;
-    bool full = A.bk_ids == nullptr || *A.log_n > A.log_cap;
-    for (int i = 0; i < len && !full; ++i) {
+    // allscan: candidates are every demand; generic: candidates split over
+    // the CTAs, every invalidated column (both rare fallbacks)
+    bool allscan = A.bk_ids == nullptr || *A.log_n > A.log_cap;
+    bool uselog = false;
+    for (int i = 0; i < len && !allscan; ++i) {
       if (S.path[i].kind != kEdgeTransfer || A.inv_cnt[i] == 0) continue;
-      if (nseg == kMaxSeg) { full = true; break; }
+      if (nseg == kMaxSeg) { allscan = true; break; }
       const int u = S.path[i].from_center;
-      nbase += A.bk_off[u + 1] - A.bk_off[u];
+      const int32_t nb = A.bk_off[u + 1] - A.bk_off[u];
+      const int32_t na = A.add_cnt != nullptr ? A.add_cnt[u] : 0;
+      if (na > A.add_cap) uselog = true;
+      nbase += nb + min(na, A.add_cap);
       if (threadIdx.x == 0) {
-        seg[2 * nseg] = i;
-        seg[2 * nseg + 1] = static_cast<int32_t>(nbase);
+        seg[3 * nseg] = i;
+        seg[3 * nseg + 1] = static_cast<int32_t>(nbase);
+        seg[3 * nseg + 2] = nb;
       }
       ++nseg;
     }
+    if (threadIdx.x == 0) S.misc[5] = 0;
+    if (threadIdx.x < kMaxSeg) { S.segmine[threadIdx.x] = 0; S.segcur[threadIdx.x] = 0; }
     __syncthreads();
-    const int64_t nlog = full ? 0 : *A.log_n;
-    int maxcnt = 0;
-    for (int i = 0; i < len; ++i) {
-      if (S.path[i].kind == kEdgeTransfer) maxcnt = max(maxcnt, A.inv_cnt[i]);
-    }
-    const int64_t ncand = full ? A.n : nbase + nlog;
-    // row mode: when a slot invalidated a good part of its row, members'
-    // cost rows are streamed (coalesced 16 B pieces, one column bitmap per
-    // slot) instead of gathering one 4 B key per (member, column)
-    const int nv = (k + 3) >> 2;
+    const int64_t nlog = (allscan || !uselog) ? 0 : *A.log_n;
+    const int64_t ncand = allscan ? A.n : nbase + nlog;
     const int nw32 = (k + 31) >> 5;
-    const bool rowmode = !full && nseg <= kRowSlots && 4 * maxcnt >= nv;
+    bool generic = allscan;
+    // my invalidated columns per segment, compacted: (g << 16) | j
+    int mycnt = 0;
+    int maxmine = 0;  // most owned columns of one segment
+    if (!generic) {
+      for (int g = 0; g < nseg; ++g) {
+        const int sl = seg[3 * g];
+        const int cnt = A.inv_cnt[sl];
+        for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+          const int j = A.inv_cols[static_cast<int64_t>(sl) * k + x];
+          if (j >= jlo && j < jhi) {
+            const int pos = atomicAdd(&S.misc[5], 1);
+            if (pos < kMaxMine) {
+              S.mine[pos] = (g << 16) | j;
+              atomicAdd(&S.segmine[g], 1);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      mycnt = S.misc[5];
+      if (mycnt > kMaxMine) generic = true;  // too many: the generic path
+    }
+    // row mode: when this CTA owns a good part of a slot's invalidations,
+    // members' cost rows are streamed over my columns (coalesced 16 B
+    // pieces, one column bitmap per segment) instead of one 4 B gather per
+    // (member, column)
+    const int p0 = jlo >> 2, p1 = (jhi + 3) >> 2;  // my 16 B pieces
+    const int npc = p1 - p0;
+    bool rowmode = false;
+    if (!generic) {
+      for (int g = 0; g < nseg; ++g) maxmine = max(maxmine, S.segmine[g]);
+      rowmode = nseg <= kRowSlots && 4 * maxmine >= npc;
+      if (rowmode) {
+        for (int w = threadIdx.x; w < nseg * nw32; w += blockDim.x) S.bits[w] = 0;
+        __syncthreads();
+        for (int x = threadIdx.x; x < mycnt; x += blockDim.x) {
+          const int g = S.mine[x] >> 16, j = S.mine[x] & 0xffff;
+          atomicOr(&S.bits[g * nw32 + (j >> 5)], 1u << (j & 31));
+        }
+      } else {
+        // group my columns by segment (counting sort; order within a
+        // segment is irrelevant)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int acc = 0;
+          for (int g = 0; g < nseg; ++g) { const int c = S.segmine[g]; S.segmine[g] = acc; acc += c; }
+          S.segmine[nseg] = acc;
+        }
+        for (int x = threadIdx.x; x < mycnt; x += blockDim.x) S.mine2[x] = S.mine[x];
+        __syncthreads();
+        for (int x = threadIdx.x; x < mycnt; x += blockDim.x) {
+          const int g = S.mine2[x] >> 16;
+          const int pos = atomicAdd(&S.segcur[g], 1);
+          S.mine[S.segmine[g] + pos] = S.mine2[x] & 0xffff;
+        }
+      }
+    }
+    const bool full = generic;
     if (X.lead) {
       A.ctl->resc[0] += 1;
       A.ctl->resc[1] += full;
       A.ctl->resc[2] += rowmode;
       A.ctl->resc[3] += ncand;
-      int64_t pairs = 0;
-      for (int i = 0; i < len; ++i) pairs += (S.path[i].kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
-      A.ctl->resc[5] += pairs;
+      A.ctl->resc[5] += total;
     }
-    if (rowmode) {
-      for (int w = threadIdx.x; w < nseg * nw32; w += blockDim.x) S.bits[w] = 0;
-      __syncthreads();
-      for (int g = 0; g < nseg; ++g) {
-        const int sl = seg[2 * g];
-        const int cnt = A.inv_cnt[sl];
-        for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
-          const int j = A.inv_cols[static_cast<int64_t>(sl) * k + x];
-          atomicOr(&S.bits[g * nw32 + (j >> 5)], 1u << (j & 31));
-        }
+    // candidates: all of them in every CTA (own columns), or split over the
+    // CTAs (every column) in the generic full mode
+    const int64_t cbase = full ? static_cast<int64_t>(X.rank) * blockDim.x : 0;
+    const int64_t stride = full ? static_cast<int64_t>(X.csz) * blockDim.x : blockDim.x;
+    int maxcnt = 0;
+    if (full) {
+      for (int i = 0; i < len; ++i) {
+        if (S.path[i].kind == kEdgeTransfer) maxcnt = max(maxcnt, A.inv_cnt[i]);
       }
     }
-    const int64_t stride = static_cast<int64_t>(X.csz) * blockDim.x;
-    for (int64_t base = static_cast<int64_t>(X.rank) * blockDim.x; base < ncand; base += stride) {
+    for (int64_t base = cbase; base < ncand; base += stride) {
       if (threadIdx.x == 0) S.misc[0] = 0;
       __syncthreads();
       const int64_t x = base + threadIdx.x;
       if (x < ncand) {
         int32_t dd = -1, sl = -1;
-        if (full) {
+        if (allscan) {
           dd = static_cast<int32_t>(x);
           const int32_t h = A.home[dd];
           if (h >= 0) {
@@ -1023,12 +1094,14 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           }
         } else if (x < nbase) {
           int g = 0;
-          while (x >= seg[2 * g + 1]) ++g;
-          const int slot = seg[2 * g];
+          while (x >= seg[3 * g + 1]) ++g;
+          const int slot = seg[3 * g];
           const int u = S.path[slot].from_center;
-          const int64_t off = x - (g == 0 ? 0 : seg[2 * g - 1]);
-          dd = A.bk_ids[A.bk_off[u] + off];
-          if (A.home[dd] == u) sl = slot;
+          const int64_t off = x - (g == 0 ? 0 : seg[3 * g - 2]);
+          const int32_t nb = seg[3 * g + 2];
+          dd = off < nb ? A.bk_ids[A.bk_off[u] + off]
+                        : A.add_ids[static_cast<int64_t>(u) * A.add_cap + (off - nb)];
+          if (A.home[dd] == u) sl = full ? slot : g;
         } else {
           const int64_t li = x - nbase;
           dd = A.log_d[li];
@@ -1036,33 +1109,52 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           if (A.home[dd] == to) {
             sl = A.rowslot[to];
             if (sl >= 0 && A.inv_cnt[sl] == 0) sl = -1;
+            if (sl >= 0 && !full) {  // slot -> segment
+              int g = 0;
+              while (g < nseg && seg[3 * g] != sl) ++g;
+              sl = g < nseg ? g : -1;
+            }
           }
         }
         if (sl >= 0) {
           const int q = atomicAdd(&S.misc[0], 1);
           S.qd[q] = dd;
-          S.qs[q] = sl;
-          S.qh[q] = A.cm[static_cast<int64_t>(dd) * A.pitch + S.path[sl].from_center];
+          S.qs[q] = sl;  // full: path slot; else: segment
+          S.qh[q] = A.cm[static_cast<int64_t>(dd) * A.pitch +
+                         S.path[full ? sl : seg[3 * sl]].from_center];
         }
       }
       __syncthreads();
       const int qn = S.misc[0];
-      if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&A.ctl->resc[4]),
-                                      static_cast<unsigned long long>(qn));
-      if (rowmode) {
-        // (member, 16 B piece) items: consecutive threads read consecutive
-        // pieces of one member's row
-        for (int p = threadIdx.x; p < qn * nv; p += blockDim.x) {
-          const int q = p / nv;
-          const int c4 = p - q * nv;
+      if (threadIdx.x == 0 && (full || X.rank == 0))
+        atomicAdd(reinterpret_cast<unsigned long long*>(&A.ctl->resc[4]),
+                  static_cast<unsigned long long>(qn));
+      if (full) {
+        // generic: (member, invalidated column) pairs over every column
+        for (int p = threadIdx.x; p < qn * maxcnt; p += blockDim.x) {
+          const int q = p % qn;
+          const int xx = p / qn;
           const int sl2 = S.qs[q];
-          int g = 0;
-          while (seg[2 * g] != sl2) ++g;
+          const int cnt = A.inv_cnt[sl2];
+          if (xx >= cnt) continue;
+          const int32_t d2 = S.qd[q];
+          const int u = S.path[sl2].from_center;
+          const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
+          const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
+          list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
+        }
+      } else if (rowmode) {
+        // (member, my 16 B piece): consecutive threads read consecutive
+        // pieces of one member's row
+        for (int p = threadIdx.x; p < qn * npc; p += blockDim.x) {
+          const int q = p / npc;
+          const int c4 = p0 + (p - q * npc);
+          const int g = S.qs[q];
           const uint32_t word = S.bits[g * nw32 + (c4 >> 3)] >> ((c4 & 7) * 4);
           if ((word & 15u) == 0) continue;
           const int32_t d2 = S.qd[q];
           const int32_t hv = S.qh[q];
-          const int u = S.path[sl2].from_center;
+          const int u = S.path[seg[3 * g]].from_center;
           const int4 x4 = reinterpret_cast<const int4*>(A.cm + static_cast<int64_t>(d2) * A.pitch)[c4];
           const int32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
@@ -1072,23 +1164,20 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
             }
           }
         }
-        __syncthreads();
-        continue;
-      }
-      // (member, invalidated column) pairs spread over every thread: two
-      // independent cost loads, then the pair's transfer sinks into the
-      // entry's emptied top-4 list (M, MX) by an atomicMin cascade
-      for (int p = threadIdx.x; p < qn * maxcnt; p += blockDim.x) {
-        const int q = p % qn;
-        const int xx = p / qn;
-        const int sl2 = S.qs[q];
-        const int cnt = A.inv_cnt[sl2];
-        if (xx >= cnt) continue;
-        const int32_t d2 = S.qd[q];
-        const int u = S.path[sl2].from_center;
-        const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
-        const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
-        list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
+      } else {
+        // (member, my invalidated column of its segment) pairs
+        for (int p = threadIdx.x; p < qn * maxmine; p += blockDim.x) {
+          const int q = p % qn;
+          const int xx = p / qn;
+          const int g = S.qs[q];
+          const int o0 = S.segmine[g], o1 = S.segmine[g + 1];
+          if (xx >= o1 - o0) continue;
+          const int j = S.mine[o0 + xx];
+          const int32_t d2 = S.qd[q];
+          const int u = S.path[seg[3 * g]].from_center;
+          const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
+          list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
+        }
       }
       __syncthreads();
     }

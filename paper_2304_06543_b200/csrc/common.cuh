@@ -162,7 +162,9 @@ struct EngineArgs {
   int32_t* log_to;
   int32_t* log_n;
   int32_t log_cap;
-  int32_t pad3;
+  int32_t add_cap;        // per-center capacity of the add lists
+  int32_t* add_ids;       // [k][add_cap]: demands that moved to center u this launch
+  int32_t* add_cnt;       // [k]: appends per center (past add_cap: use the move log)
   int64_t* MX;            // k*k*3: 2nd..4th smallest transfer per entry
   uint8_t* LN;            // k*k: list length | complete << 3
   int32_t debug_checks;   // validate engine invariants after each phase

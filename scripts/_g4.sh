@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/g4_pytest.log 2>&1; echo "pytest rc $?" >> gpurun_out/g4_pytest.log; tail -3 gpurun_out/g4_pytest.log
+timeout 200 python scripts/repro_small.py > gpurun_out/g4_repro.log 2>&1; echo "repro rc $?"; tail -1 gpurun_out/g4_repro.log
+LBDD_B200_PROF=1 python scripts/solve_one.py --n 200000 > gpurun_out/g4_200k_prof.log 2>&1; cut -c1-1500 gpurun_out/g4_200k_prof.log

@@ -122,7 +122,9 @@ long long lbdd_b200_launch_count(void);
  * out[9] path searches pruned by the penalty bound, out[10..12] rounds per
  * kind, out[13..15] path-bound statistics; out[16..31] cluster-engine
  * lead-thread cycles per phase; out[32..37] rescans (calls, full scans,
- * row-mode, candidates, members, member-column pairs). out has 40 slots. */
+ * row-mode, candidates, members, member-column pairs). out[40..55] / out[56..71]
+ * per-CTA work / barrier-wait cycles between exchanges (LBDD_B200_PROF=1).
+ * out has 72 slots. */
 void lbdd_b200_engine_counters(int64_t* out);
 
 /* Upload an instance (host arrays) to `device`. Replaces constructing a

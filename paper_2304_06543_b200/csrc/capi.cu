@@ -672,7 +672,7 @@ size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
          2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) + 8 * (k + 1) +
          4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * static_cast<size_t>(cl::kMaxCS) * s + 4 * 3 * cl::kMaxSeg +
          4 * 2 * cl::kMaxMine + 4 * (2 * cl::kMaxSeg + 2) +
-         8 * 16 + 8 * 16 +
+         8 * 16 + 8 * 16 + 8 * 4 +
          sizeof(PathEdge) * (k + 1) + 12 * block + 4 * 16 +
          4 * static_cast<size_t>(cl::kRowSlots) * ((k + 31) / 32) +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
@@ -1093,6 +1093,8 @@ void lbdd_b200_engine_counters(int64_t* out) {
   for (int i = 0; i < 16; ++i) out[i] = g_last_ctl.dbg[i];
   for (int i = 0; i < 16; ++i) out[16 + i] = g_last_ctl.prof[i];
   for (int i = 0; i < 8; ++i) out[32 + i] = g_last_ctl.resc[i];
+  for (int i = 0; i < 16; ++i) out[40 + i] = g_last_ctl.cta_work[i];
+  for (int i = 0; i < 16; ++i) out[56 + i] = g_last_ctl.cta_wait[i];
 }
 const char* lbdd_b200_last_error(void) { return g_err.c_str(); }
 

@@ -118,6 +118,7 @@ struct CS {           // shared-memory layout of one CTA
   int32_t* segcur;    // [kMaxSeg] counting-sort cursors
   int64_t* dbg;       // [16] instrumentation counters
   int64_t* prof;      // [16] lead-thread cycle counters per phase
+  int64_t* cw;        // [4] per-CTA profile: last exchange, work cycles, wait cycles
   int16_t* wt;        // [k * s] transfer keys of every row into my columns
                       // (tile mode: all keys fit in int16)
 };
@@ -144,6 +145,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.segcur = reinterpret_cast<int32_t*>(p); p += 4 * kMaxSeg;
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
+  S.cw = reinterpret_cast<int64_t*>(p); p += 8 * 4;
   S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
   S.qd = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
   S.qs = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
@@ -194,7 +196,19 @@ __device__ __forceinline__ int32_t pair_kind(int64_t m, bool dummy) {
   if (dummy && (m == kEmpty || transfer_key(m) >= 0)) return kEdgeDummy;
   return m == kEmpty ? kEdgeNone : kEdgeTransfer;
 }
-__device__ __forceinline__ int64_t lab_d(int64_t lab) { return lab >> kCandShift; }
+// Search labels pack (d, h, parent): d (reduced distance) << 26 | h (hops)
+// << 13 | parent node. Signed 64-bit order is lexicographic (d, h, parent),
+// so one atomicMin per candidate keeps, among the shortest candidates with
+// the fewest hops, the smallest parent -- the synchronous Bellman-Ford
+// parent rule of parallel.hpp:145-169. Nodes < 8192.
+constexpr int kHopShift = 13;
+constexpr int kLabShift = 26;
+constexpr int64_t kHop = int64_t(1) << kHopShift;
+constexpr int64_t kLUnit = int64_t(1) << kLabShift;
+constexpr int64_t kParMask = kHop - 1;
+constexpr int64_t kPiLimit = int64_t(1) << 35;  // |π| bound: lp = label + π << 26 fits int64
+__device__ __forceinline__ int64_t lab_d(int64_t lab) { return lab >> kLabShift; }
+__device__ __forceinline__ int32_t lab_parent(int64_t lab) { return static_cast<int32_t>(lab & kParMask); }
 __device__ __forceinline__ int16_t key16(int64_t m) {
   return m == kEmpty ? kNoKey16 : static_cast<int16_t>(transfer_key(m));
 }
@@ -203,7 +217,7 @@ __device__ __forceinline__ int64_t key16_weight(int16_t key, bool dummy) {
   return key == kNoKey16 ? kNoEdge : static_cast<int64_t>(key);
 }
 __device__ __forceinline__ int32_t lab_h(int64_t lab) {
-  return static_cast<int32_t>(lab & ((int64_t(1) << kCandShift) - 1));
+  return static_cast<int32_t>((lab >> kHopShift) & kParMask);
 }
 
 enum SearchKind : int32_t { kCycle = 0, kPath = 1, kRepair = 2 };
@@ -437,7 +451,17 @@ __device__ __forceinline__ void exchange(Ctx& X) {
       dst[X.rank] = *S.pub[X.par];
     }
   }
+  long long tw0 = 0;
+  if (X.A.profile && threadIdx.x == 0) {
+    tw0 = clock64();
+    S.cw[1] += tw0 - S.cw[0];  // work since the last exchange (this CTA)
+  }
   X.cluster.sync();
+  if (X.A.profile && threadIdx.x == 0) {
+    const long long t1 = clock64();
+    S.cw[2] += t1 - tw0;       // waited at the barrier (this CTA)
+    S.cw[0] = t1;
+  }
   S.all = S.allb[X.par];
   if (threadIdx.x < 32) {
     // warp 0: scan the counts, OR the errors
@@ -520,7 +544,7 @@ __device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label
   FEntry e;
   e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
   e.pad = 0;
-  e.lp = label + pi * (int64_t(1) << kCandShift);
+  e.lp = ((label & ~kParMask) | v) + pi * kLUnit;  // a candidate's parent field = v
   const int slot = X.rank * X.s + pos;
   for (int r = 0; r < X.csz; ++r) {
     FEntry* box = X.cluster.map_shared_rank(X.S.inbox[X.par], r);
@@ -578,27 +602,41 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
   const int ns = X.v1 - X.v0;
   if (ns <= 0) return;  // uniform within the CTA
   const int cpp = X.cpp, rpp = X.rpp, tx = X.tx, ty = X.ty;
-  constexpr int64_t kUnit = int64_t(1) << kCandShift;
+  constexpr int64_t kUnit = kLUnit;
+  const int cnt_all = S.pref[X.csz];
+  if (kind != kRepair && X.k >= X.v0 && X.k < X.v1) {
+    // anchor-in (sink) column: its weights come from S.sinkw, not the tile.
+    // Evaluated by the whole CTA in a separate pass, so no warp of the
+    // column loop below diverges into a second, scalar branch.
+    const int col = X.k - X.v0;
+    const int64_t base = kHop - S.pis[col] * kUnit;
+    int64_t best = kLabInf;
+    for (int t = threadIdx.x; t < cnt_all; t += blockDim.x) {
+      const FEntry e = S.cmp[t];
+      const int64_t w = S.sinkw[fe_node(e)];  // kNoEdge for the anchor itself
+      if (w == kNoEdge) continue;
+      const int64_t cand = e.lp + w * kUnit + base;
+      if (cand < bound_sink && cand < best) best = cand;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0 && best != kLabInf) {
+      const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
+                                      static_cast<long long>(best));
+      if ((best & ~kParMask) < (old & ~kParMask)) S.chg[col] = 1;
+    }
+  }
   for (int c0 = 0; c0 < ns; c0 += cpp) {
     const int col = c0 + tx;
     const int v = X.v0 + col;
     if (col >= ns) continue;
-    const bool sinkcol = kind != kRepair && v == X.k;
-    if (v > X.k || (kind != kRepair && v == anchor) || (kind == kRepair && v == X.k)) continue;
-    const int64_t base = 1 - S.pis[col] * kUnit;  // candidate = lp + w*unit + base
-    const int64_t bound = sinkcol ? bound_sink : bound_mid;
+    if (v >= X.k || (kind != kRepair && v == anchor)) continue;
+    const int64_t base = kHop - S.pis[col] * kUnit;  // candidate = lp + w*unit + base
+    const int64_t bound = bound_mid;
     int64_t best = kLabInf;
     const int cnt = S.pref[X.csz];
     const FEntry* cmp = S.cmp;
-    if (sinkcol) {
-      for (int t = ty; t < cnt; t += rpp) {
-        const FEntry e = cmp[t];
-        const int64_t w = S.sinkw[fe_node(e)];  // kNoEdge for the anchor itself
-        if (w == kNoEdge) continue;
-        const int64_t cand = e.lp + w * kUnit + base;
-        if (cand < bound && cand < best) best = cand;
-      }
-    } else if (X.tile && X.A.dummies == nullptr) {
+    if (X.tile && X.A.dummies == nullptr) {
       // asral: no placeholder flags. cand < min(bound, best) is tested as
       // lp + w * unit < lim with lim = min(bound, best) - base, shrinking
       const int16_t* wcol = S.wt + col;
@@ -660,7 +698,9 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
     if (best != kLabInf) {
       const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
                                       static_cast<long long>(best));
-      if (best < old) S.chg[col] = 1;
+      // a better parent alone changes nothing downstream: re-push only on
+      // a smaller (d, h)
+      if ((best & ~kParMask) < (old & ~kParMask)) S.chg[col] = 1;
     }
   }
 }
@@ -690,7 +730,10 @@ __device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, 
 __device__ __forceinline__ bool sink_settled(const Ctx& X, int64_t sink_inc) {
   if (sink_inc == kLabInf) return false;
   const int64_t sl = X.S.agg->sinklab, om = X.S.agg->omin;
-  return sl != kLabInf && (om == kLabInf || om + sink_inc > sl);
+  // a candidate into the sink from an open node x has (d, h) part >=
+  // (d, h)(x) + sink_inc; the parent field of an equal (d, h) could still
+  // lower the sink, so settle only on a strictly larger (d, h)
+  return sl != kLabInf && (om == kLabInf || (om & ~kParMask) + sink_inc > (sl & ~kParMask));
 }
 
 __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
@@ -769,107 +812,75 @@ __device__ __forceinline__ void apply_repair(Ctx& X) {
     const int64_t d = lab_d(l);
     if (d < 0) {
       X.S.pis[i] += d;
-      if (X.S.pis[i] < -(int64_t(1) << 44)) set_err(X, kErrOverflow, X.v0 + i);
+      if (X.S.pis[i] < -kPiLimit) set_err(X, kErrOverflow, X.v0 + i);
     }
   }
   X.cluster.sync();
 }
 
-// Parent walk (refine.hpp:53-80) with the synchronous-BF parent rule:
-// parent(v) = min u with lab(u) + rc(u,v)*2^16 + 1 == lab(v). Fills S.path
-// (in path order) and returns its length; 0 + error on a broken chain.
+// Parent walk (refine.hpp:53-80). The parent rule of the synchronous BF is
+// already in the labels (their parent field, see lab_parent), so every CTA
+// walks the chain from anchor-in back to anchor-out itself, reading the
+// labels of the path nodes from their owners through DSMEM, then reads the
+// transfer word of each edge. One exchange at the end: past it, T1 of
+// faster CTAs rewrites the lists the words were read from. Fills S.path in
+// path order and returns its length (0 + error on a broken chain).
 __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t sinklab) {
   CS& S = X.S;
   const EngineArgs& A = X.A;
-  int v = X.k;
-  int64_t lv = sinklab;
-  int64_t piv = pi_of(X, anchor);  // π(anchor-in) = π(anchor)
-  int len = 0;
-  while (v != anchor) {
-    if (len > X.k) { set_err(X, kErrPathNotSimple, len); break; }
-    // smallest owned explored u whose edge into v is tight
-    int64_t best = kEmpty;
-    for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
-      const int u = X.v0 + i;
-      if (u == X.k || u == v) continue;
-      const int64_t lu = S.lab[i];
-      if (lu == kLabInf) continue;
-      int64_t w;
-      const bool dum = kind == kCycle && has_dummy(X, u);
-      if (v == X.k) {
-        if (u == anchor) continue;
-        w = kind == kCycle ? pair_weight(A.M[static_cast<int64_t>(u) * A.k + anchor], dum)
-                           : marginal_penalty(X, u, A.load[u]) - refund_a;
-      } else {
-        if (v == anchor) continue;
-        w = pair_weight(A.M[static_cast<int64_t>(u) * A.k + v], dum);
-      }
-      if (w == kNoEdge) continue;
-      const int64_t rc = w + S.pis[i] - piv;
-      if (lu + rc * (int64_t(1) << kCandShift) + 1 != lv) continue;
-      best = min(best, static_cast<int64_t>(u));
-    }
-    if (threadIdx.x == 0) S.red[0] = kEmpty;
-    __syncthreads();
-    atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(best));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      Pub* p = S.pub[X.par];
-      const int64_t bu = S.red[0];
-      p->val = bu;
-      p->count = 0;
-      p->sinklab = bu == kEmpty ? kLabInf : S.lab[bu - X.v0];  // the parent's label
-      // the edge's transfer word, read BEFORE the barrier: past it, CTAs
-      // that finished reconstructing may already rewrite M in apply (T1)
-      const int cv = v == X.k ? anchor : v;
-      p->pmin = (bu == kEmpty || (kind == kPath && v == X.k))
-                    ? kEmpty : A.M[bu * static_cast<int64_t>(A.k) + cv];
-    }
-    exchange(X);
-    int64_t u = kEmpty;
-    int64_t lu = 0;
-    int64_t word = kEmpty;
-    for (int r = 0; r < X.csz; ++r) {
-      if (S.all[r].val < u) {
-        u = S.all[r].val;
-        lu = S.all[r].sinklab;
-        word = S.all[r].pmin;
-      }
-    }
-    if (u == kEmpty) { set_err(X, kErrBrokenParent, v); X.err = 1; break; }
-    // record edge u -> v (reversed order for now)
-    if (threadIdx.x == 0) {
-      PathEdge e;
-      const int uu = static_cast<int>(u);
-      const int cv = v == X.k ? anchor : v;
-      e.from_center = uu;
-      e.to_center = cv;
-      e.demand = -1;
-      if (kind == kPath && v == X.k) {
-        e.kind = kEdgePenalty;
-      } else {
-        const int64_t m = word;
-        const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[uu] > 0;
-        e.kind = pair_kind(m, dum);
-        if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
-      }
-      S.path[len] = e;
-    }
-    piv = pi_of(X, static_cast<int>(u));
-    lv = lu;
-    v = static_cast<int>(u);
-    ++len;
-    __syncthreads();
-  }
-  // reverse into path order
   if (threadIdx.x == 0) {
+    int v = X.k;
+    int64_t lv = sinklab;
+    int len = 0;
+    int bad = 0;
+    while (v != anchor) {
+      if (len > X.k) { bad = kErrPathNotSimple; break; }
+      const int u = lab_parent(lv);
+      if (u >= X.k || u == v || lv == kLabInf) { bad = kErrBrokenParent; break; }
+      PathEdge e;
+      e.from_center = u;
+      e.to_center = v == X.k ? anchor : v;
+      e.demand = -1;
+      e.kind = kEdgeNone;
+      S.path[len++] = e;  // reversed order for now
+      if (u != anchor) {
+        const int r = u / X.s;
+        lv = X.cluster.map_shared_rank(S.lab, r)[u - r * X.s];
+      }
+      v = u;
+    }
+    S.misc[6] = bad ? -bad : len;
+  }
+  __syncthreads();
+  const int len = S.misc[6];
+  if (len <= 0) {
+    if (X.lead) set_err(X, -len, 0);
+    X.err = 1;
+    return 0;
+  }
+  // edge kinds and transfer words (the first recorded edge enters anchor-in)
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    PathEdge e = S.path[i];
+    if (kind == kPath && i == 0) {
+      e.kind = kEdgePenalty;
+    } else {
+      const int64_t m = A.M[static_cast<int64_t>(e.from_center) * A.k + e.to_center];
+      const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[e.from_center] > 0;
+      e.kind = pair_kind(m, dum);
+      if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
+    }
+    S.path[i] = e;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // reverse into path order
     for (int i = 0; i < len / 2; ++i) {
       const PathEdge t = S.path[i];
       S.path[i] = S.path[len - 1 - i];
       S.path[len - 1 - i] = t;
     }
+    S.pub[X.par]->count = 0;
   }
-  __syncthreads();
+  exchange(X);
   return X.err ? 0 : len;
 }
 
@@ -1254,7 +1265,7 @@ __device__ __forceinline__ bool finish_search(Ctx& X, int kind, int anchor, int6
   const int64_t t0 = gtimer();
   // smallest possible increment of an edge into anchor-in, in packed units:
   // cycle graph rc >= 0; path graph rc_pen >= C = -bound_mid (see caller)
-  const int64_t sink_inc = kind == kCycle ? 1 : 1 - bound_mid;
+  const int64_t sink_inc = kind == kCycle ? kHop : kHop - bound_mid;
   const int rounds = search_rounds(X, kind, anchor, refund_a, bound_mid, 0, sink_inc);
   const int64_t sl = sink_label(X);
   if (X.lead) {
@@ -1359,13 +1370,14 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   X.lead = X.rank == 0 && threadIdx.x == 0;
   X.n_barriers = 0;
   X.n_rounds = 0;
-  X.delta_main = A.delta_step <= 0 ? kLabInf / 4 : (A.delta_step << kCandShift);
-  X.delta_path = A.delta_path <= 0 ? kLabInf / 4 : (A.delta_path << kCandShift);
+  X.delta_main = A.delta_step <= 0 ? kLabInf / 4 : (A.delta_step << kLabShift);
+  X.delta_path = A.delta_path <= 0 ? kLabInf / 4 : (A.delta_path << kLabShift);
   X.delta = X.delta_main;
   X.T = X.delta;
   X.dbg = X.S.dbg;
   if (threadIdx.x < 16) X.dbg[threadIdx.x] = 0;
   if (threadIdx.x < 16) X.S.prof[threadIdx.x] = 0;
+  if (threadIdx.x < 4) X.S.cw[threadIdx.x] = threadIdx.x == 0 ? clock64() : 0;
   CS& S = X.S;
   const int k = A.k;
   const bool strict = A.mode == 1;
@@ -1396,6 +1408,32 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   }
   __syncthreads();
   X.cluster.sync();
+  // renormalise π so that its maximum is 0: reduced costs are invariant
+  // under a uniform shift, and repairs only ever lower π, so without this it
+  // would drift towards the packing limit over a long solve
+  {
+    if (threadIdx.x == 0) S.red[1] = INT64_MIN;
+    __syncthreads();
+    long long mx = INT64_MIN;
+    for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+      if (X.v0 + i < k) mx = max(mx, static_cast<long long>(S.pis[i]));
+    }
+    atomicMax(reinterpret_cast<long long*>(&S.red[1]), mx);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.pub[X.par]->val = S.red[1];
+      S.pub[X.par]->count = 0;
+    }
+    exchange(X);
+    int64_t gmax = INT64_MIN;
+    for (int r = 0; r < X.csz; ++r) gmax = max(gmax, S.all[r].val);
+    if (gmax != INT64_MIN) {
+      for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+        if (X.v0 + i < k) S.pis[i] -= gmax;
+      }
+    }
+    __syncthreads();
+  }
   int* dirty = dirty_buf + X.rank * (2 * k + 4);  // per-CTA scratch
 
   PROF_MARK(X, 14);
@@ -1473,7 +1511,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         const int64_t w = pair_weight(m, strict && dum_a);
         if (w != kNoEdge) {
           const int64_t rc = w + pi_s - S.pis[j - X.v0];
-          const int64_t cand = rc * (int64_t(1) << kCandShift) + 1;
+          const int64_t cand = rc * kLUnit + kHop + s;  // parent s
           if (cand < 0) {
             S.lab[j - X.v0] = cand;
             S.chg[j - X.v0] = 1;
@@ -1566,7 +1604,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         __syncthreads();
         exchange(X);
         int nd2 = 0;
-        const int64_t bound = (-C) * (int64_t(1) << kCandShift);
+        const int64_t bound = (-C) * kLUnit;
         PROF_MARK(X, 6);
         applied = finish_search(X, kPath, s, refund, bound, dirty, &nd2);
         X.delta = X.delta_main;
@@ -1585,6 +1623,10 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     A.ctl->barriers += X.n_barriers;
     A.ctl->relax_rounds += X.n_rounds;
 
+  }
+  if (A.profile && threadIdx.x == 0) {
+    A.ctl->cta_work[X.rank] += S.cw[1];
+    A.ctl->cta_wait[X.rank] += S.cw[2];
   }
   // persist π for the next launch
   __syncthreads();

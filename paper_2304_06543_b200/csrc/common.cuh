@@ -89,6 +89,8 @@ struct EngineCtl {
   int64_t prof[16];               // cluster engine: lead-thread cycles per phase
   int64_t resc[8];                // cluster engine rescans: calls, full-scan, row-mode,
                                   // candidates, members, (member, column) pairs
+  int64_t cta_wait[16];           // cluster engine (profile): cycles each CTA waited in exchanges
+  int64_t cta_work[16];           // cluster engine (profile): cycles between exchanges per CTA
   int32_t error;
   int32_t error_arg;
   int32_t prev_sources;           // transfer sources of the last applied path

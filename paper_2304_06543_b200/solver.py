@@ -82,7 +82,7 @@ def launch_count() -> int:
 
 def engine_counters():
     """Instrumentation of the last solve (see include/lbdd_b200.h)."""
-    out = np.zeros(40, np.int64)
+    out = np.zeros(72, np.int64)
     _lib.lbdd_b200_engine_counters(_i64(out))
     names = ["cycle_searches", "path_searches", "repair_searches", "cycle_empty", "path_empty",
              "repair_empty", "cycle_frontier", "path_frontier", "repair_frontier", "path_pruned",
@@ -94,6 +94,8 @@ def engine_counters():
     d["cycles"] = {p: int(out[16 + i]) for i, p in enumerate(phases)}
     d["rescans"] = {p: int(out[32 + i]) for i, p in enumerate(
         ["calls", "full", "row_mode", "candidates", "members", "pairs"])}
+    d["cta_work"] = [int(x) for x in out[40:56]]
+    d["cta_wait"] = [int(x) for x in out[56:72]]
     return d
 
 

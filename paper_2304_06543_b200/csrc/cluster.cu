@@ -73,6 +73,10 @@ struct Pub {          // per-CTA published scalars of one exchange
   int64_t omin;       // smallest open label (held back or pushed this round)
 };
 
+
+static_assert(sizeof(Pub) == 48, "Pub travels as three 16 B st.async");
+static_assert(sizeof(FEntry) == 16, "FEntry travels as one 16 B st.async");
+
 struct Agg {          // cluster-wide reductions of the last exchange (warp 0)
   int32_t pending;    // sum of Pub::pending
   int32_t pad;
@@ -119,6 +123,7 @@ struct CS {           // shared-memory layout of one CTA
   int64_t* dbg;       // [16] instrumentation counters
   int64_t* prof;      // [16] lead-thread cycle counters per phase
   int64_t* cw;        // [4] per-CTA profile: last exchange, work cycles, wait cycles
+  uint64_t* rmb;      // [2] round mbarriers (by parity): csz arrivals + st.async bytes
   int16_t* wt;        // [k * s] transfer keys of every row into my columns
                       // (tile mode: all keys fit in int16)
 };
@@ -146,6 +151,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.cw = reinterpret_cast<int64_t*>(p); p += 8 * 4;
+  S.rmb = reinterpret_cast<uint64_t*>(p); p += 8 * 2;
   S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
   S.qd = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
   S.qs = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
@@ -228,6 +234,7 @@ struct Ctx {
   cg::cluster_group cluster;
   int rank, csz, k, s, v0, v1;
   int par;
+  unsigned rph;       // phase bits of the round mbarriers S.rmb[0], S.rmb[1]
   int err;            // sticky, identical in all CTAs (read at exchanges)
   bool lead;          // rank 0, thread 0
   bool tile;          // keys of my columns resident in S.wt
@@ -432,10 +439,43 @@ __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
   return X.A.dummies != nullptr && X.A.dummies[u] > 0;
 }
 
+// ---- st.async round exchange (search rounds) ----
+// A search round moves only shared-memory data between CTAs (frontier
+// entries and the published scalars), so it does not need the cluster
+// barrier's release/acquire of global memory (a GPU-scope MEMBAR plus an L1
+// invalidate per barrier). Each CTA writes into every CTA's inbox[par] /
+// allb[par] with st.async, whose bytes complete_tx on the destination's
+// round mbarrier rmb[par]; after its last store to a destination it arrives
+// there (relaxed, remote) declaring the bytes it sent. A CTA's round is over
+// when all csz CTAs arrived and all declared bytes landed. 676 vs 1607
+// cycles per exchange in isolation (scripts/latency_floor.py).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async16(unsigned raddr, const void* src, unsigned rbar) {
+  const int4 v = *reinterpret_cast<const int4*>(src);
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(raddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void remote_arrive_tx(unsigned rbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;"
+               ::"r"(rbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+  asm volatile("{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra W%=;\n}" ::"r"(bar), "r"(phase) : "memory");
+}
+
 // Cluster barrier + exchange: every CTA publishes pub[par] (count, err,
 // sink label, reduction slot) — and pushes inbox[par] — before calling;
 // afterwards S.all[] holds the values of every CTA, identical everywhere,
 // and par flips, so inbox[par ^ 1] holds the sources of the next relaxation.
+__device__ __forceinline__ void exchange_finish(Ctx& X);
 __device__ __forceinline__ void exchange(Ctx& X) {
   CS& S = X.S;
   if (threadIdx.x < 32) {
@@ -462,6 +502,46 @@ __device__ __forceinline__ void exchange(Ctx& X) {
     S.cw[2] += t1 - tw0;       // waited at the barrier (this CTA)
     S.cw[0] = t1;
   }
+  exchange_finish(X);
+}
+
+// The round variant: entries were pushed by collect(async) with st.async;
+// warp 0 sends the pub and arrives at every CTA, then all threads wait.
+__device__ __forceinline__ void exchange_async(Ctx& X) {
+  CS& S = X.S;
+  const unsigned bar = smem_u32(&S.rmb[X.par]);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) S.pub[X.par]->err = S.misc[2];
+    __syncwarp();
+    if (threadIdx.x < X.csz) {
+      const int r = static_cast<int>(threadIdx.x);
+      const Pub* mine = S.pub[X.par];
+      const unsigned rbar = mapa_u32(bar, r);
+      const unsigned dst = mapa_u32(smem_u32(&S.allb[X.par][X.rank]), r);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        st_async16(dst + 16 * q, reinterpret_cast<const char*>(mine) + 16 * q, rbar);
+      }
+      remote_arrive_tx(rbar, static_cast<unsigned>(sizeof(Pub) + sizeof(FEntry) * mine->count));
+    }
+  }
+  long long tw0 = 0;
+  if (X.A.profile && threadIdx.x == 0) {
+    tw0 = clock64();
+    S.cw[1] += tw0 - S.cw[0];
+  }
+  mbar_wait(bar, (X.rph >> X.par) & 1u);
+  X.rph ^= 1u << X.par;
+  if (X.A.profile && threadIdx.x == 0) {
+    const long long t1 = clock64();
+    S.cw[2] += t1 - tw0;
+    S.cw[0] = t1;
+  }
+  exchange_finish(X);
+}
+
+__device__ __forceinline__ void exchange_finish(Ctx& X) {
+  CS& S = X.S;
   S.all = S.allb[X.par];
   if (threadIdx.x < 32) {
     // warp 0: scan the counts, OR the errors
@@ -552,9 +632,20 @@ __device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label
   }
 }
 
+__device__ __forceinline__ void push_entry_async(Ctx& X, int pos, int v, int64_t label, int64_t pi,
+                                                 bool dum) {
+  FEntry e;
+  e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
+  e.pad = 0;
+  e.lp = ((label & ~kParMask) | v) + pi * kLUnit;
+  const unsigned src = smem_u32(&X.S.inbox[X.par][X.rank * X.s + pos]);
+  const unsigned bar = smem_u32(&X.S.rmb[X.par]);
+  for (int r = 0; r < X.csz; ++r) st_async16(mapa_u32(src, r), &e, mapa_u32(bar, r));
+}
+
 // Δ-stepping: only improved nodes with label <= X.T are pushed; the rest
 // stay pending (their flag kept) and report their count and minimum.
-__device__ __forceinline__ void collect(Ctx& X, int kind, int anchor) {
+__device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async = false) {
   CS& S = X.S;
   if (threadIdx.x == 0) {
     S.misc[1] = 0;
@@ -576,7 +667,8 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor) {
     S.chg[i] = 0;
     atomicMin(reinterpret_cast<long long*>(&S.red[3]), static_cast<long long>(label));
     const int pos = atomicAdd(&S.misc[1], 1);
-    push_entry(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
+    if (async) push_entry_async(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
+    else push_entry(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
     if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
   }
   __syncthreads();
@@ -750,9 +842,9 @@ __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64
     relax(X, kind, anchor, refund_a, bound_mid, bound_sink);
     __syncthreads();
     PROF_MARK(X, 1);
-    collect(X, kind, anchor);
+    collect(X, kind, anchor, true);
     PROF_MARK(X, 2);
-    exchange(X);
+    exchange_async(X);
     advance_threshold(X);
     PROF_MARK(X, 3);
     ++rounds;
@@ -1274,6 +1366,10 @@ __device__ __forceinline__ bool finish_search(Ctx& X, int kind, int anchor, int6
   }
   *nd = 0;
   if (X.err || sl == kLabInf || lab_d(sl) >= 0) return false;
+  // the rounds' st.async exchanges do not release the owners' label writes;
+  // reconstruct reads labels through DSMEM, so fence them with one barrier
+  X.cluster.sync();
+  if (X.lead) X.n_barriers += 1;
   PROF_MARK(X, 9);
   // invalidation counters of the previous apply: its readers finished
   // before the last barrier, the next writers (T1) come after the next one
@@ -1398,6 +1494,12 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     }
   }
   if (threadIdx.x < 16) S.misc[threadIdx.x] = 0;
+  X.rph = 0;
+  if (threadIdx.x < 2) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&S.rmb[threadIdx.x])),
+                 "r"(X.csz));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       S.pub[b]->count = 0;
@@ -1655,9 +1757,46 @@ __global__ void __launch_bounds__(512, 1) cluster_exchange_bench(int iters, int 
   if (threadIdx.x < 128) list[threadIdx.x].nd = threadIdx.x;
   if (threadIdx.x == 0) { pub[0].count = 1; pub[1].count = 1; }
   cluster.sync();
+  __shared__ __align__(8) unsigned long long mbar[2];
+  __shared__ __align__(16) int4 box[2][cl::kMaxCS];
+  if (threadIdx.x < 2) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(csz));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  cluster.sync();
   const long long t0 = clock64();
   int par = 0;
   int acc = 0;
+  unsigned phase[2] = {0, 0};
+  if (mode & 8) {
+    // st.async + mbarrier exchange: lane r of warp 0 sends this CTA's 16 B
+    // record into slot `rank` of CTA r and arrives on r's mbarrier with the
+    // byte count; thread 0 waits on the local mbarrier's phase
+    const unsigned rank = cluster.block_rank();
+    for (int it = 0; it < iters; ++it) {
+      if (threadIdx.x < csz) {
+        const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&box[par][rank]));
+        const unsigned lm = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[par]));
+        unsigned rb, rm;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(threadIdx.x));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rm) : "r"(lm), "r"(threadIdx.x));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                     ::"r"(rb), "r"(it), "r"(1), "r"(2), "r"(3), "r"(rm) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;"
+                     ::"r"(rm), "r"(16) : "memory");
+      }
+      if (threadIdx.x == 0) {
+        const unsigned lm = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[par]));
+        asm volatile("{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+                     " @!p bra W%=;\n}" ::"r"(lm), "r"(phase[par]) : "memory");
+      }
+      phase[par] ^= 1;
+      __syncthreads();
+      acc += box[par][it % csz].x;
+      par ^= 1;
+    }
+  } else
   for (int it = 0; it < iters; ++it) {
     if (mode & 1) {
       if (threadIdx.x < 128) {
@@ -1668,7 +1807,10 @@ __global__ void __launch_bounds__(512, 1) cluster_exchange_bench(int iters, int 
       acc += stage[threadIdx.x & 127].nd;
     }
     if (threadIdx.x == 0) pub[par].count = it;
-    if (mode & 2) {
+    if (mode & 4) {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    } else if (mode & 2) {
       asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
       asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     } else {

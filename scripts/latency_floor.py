@@ -19,13 +19,15 @@ clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,nohea
 mhz = float(clk) if clk.replace(".", "").isdigit() else 1965.0
 out = {}
 for cs in (16, 8):
-    for mode in (0, 1):
+    for mode in (0, 1, 2, 4, 8):
         cyc = min(S._lib.lbdd_b200_debug_exchange_cycles(cs, 20000, mode) for _ in range(3))
         out[f"cs{cs}_mode{mode}_cycles"] = cyc
 mx = 1965.0
 res = {"barrier_exchange_cycles": out["cs16_mode0_cycles"],
        "barrier_exchange_us": round(out["cs16_mode0_cycles"] / mx, 4),
        "barrier_exchange_staged_us": round(out["cs16_mode1_cycles"] / mx, 4),
+       "relaxed_barrier_us": round(out["cs16_mode4_cycles"] / mx, 4),
+       "st_async_mbarrier_us": round(out["cs16_mode8_cycles"] / mx, 4),
        "all": out, "sm_mhz_sampled": mhz,
        "source": "scripts/latency_floor.py: cluster_exchange_bench (cluster.cu), 16 CTAs x 512 "
                  "threads, clock64 cycles per round / 1965 MHz"}

@@ -1312,19 +1312,6 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   return nd;
 }
 
-// π repair from the rows in `dirty` (sources with label 0, bound 0).
-__device__ __forceinline__ void repair(Ctx& X, const int* dirty, int nd) {
-  reset_labels(X, 0);
-  __syncthreads();
-  publish_sources(X, dirty, nd, kRepair);
-  __syncthreads();
-  exchange(X);
-  const int rounds = search_rounds(X, kRepair, -1, 0, 0, 0);
-  apply_repair(X);
-  __syncthreads();
-  if (X.lead) X.n_rounds += rounds;
-}
-
 // check_invariants: π feasible on every Γ edge certifies "no negative
 // cycle" (refine.hpp:125-131). Owners check the edges into their nodes.
 __device__ __forceinline__ void certify(Ctx& X) {
@@ -1349,87 +1336,28 @@ __device__ __forceinline__ void certify(Ctx& X) {
   exchange(X);
 }
 
-// One refinement (cycle or path) at `anchor` after the sources are
-// published and exchanged. Returns applied; `dirty` gets the rows to
-// repair when applied.
-__device__ __forceinline__ bool finish_search(Ctx& X, int kind, int anchor, int64_t refund_a, int64_t bound_mid,
-                              int* dirty, int* nd) {
-  const int64_t t0 = gtimer();
-  // smallest possible increment of an edge into anchor-in, in packed units:
-  // cycle graph rc >= 0; path graph rc_pen >= C = -bound_mid (see caller)
-  const int64_t sink_inc = kind == kCycle ? kHop : kHop - bound_mid;
-  const int rounds = search_rounds(X, kind, anchor, refund_a, bound_mid, 0, sink_inc);
-  const int64_t sl = sink_label(X);
-  if (X.lead) {
-    X.n_rounds += rounds;
-    X.A.ctl->t_bf_ns += gtimer() - t0;
-  }
-  *nd = 0;
-  if (X.err || sl == kLabInf || lab_d(sl) >= 0) return false;
-  // the rounds' st.async exchanges do not release the owners' label writes;
-  // reconstruct reads labels through DSMEM, so fence them with one barrier
-  X.cluster.sync();
-  if (X.lead) X.n_barriers += 1;
-  PROF_MARK(X, 9);
-  // invalidation counters of the previous apply: its readers finished
-  // before the last barrier, the next writers (T1) come after the next one
-  if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i <= X.k; i += blockDim.x) X.A.inv_cnt[i] = 0;
-  }
-  const int len = reconstruct(X, kind, anchor, refund_a, sl);
-  PROF_MARK(X, 10);
-  if (len == 0 || X.err) return false;
-  if (kind == kPath && X.S.path[len - 1].kind != kEdgePenalty) {
-    if (X.lead) set_err(X, kErrPenaltyEdge, len);
-    X.err = 1;
-    return false;
-  }
-  // the reference checks the path's edge sum against its cost
-  // (refine.hpp:75-79): recount it from the cost matrix (one lookup per
-  // edge), so a stale transfer weight can never reach the objective
-  if (X.lead) {
-    const EngineArgs& A = X.A;
-    int64_t sum = 0;
-    for (int i = 0; i < len; ++i) {
-      const PathEdge e = X.S.path[i];
-      if (e.kind == kEdgeTransfer) {
-        const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
-        sum += static_cast<int64_t>(row[e.to_center]) - row[e.from_center];
-      } else if (e.kind == kEdgePenalty) {
-        sum += marginal_penalty(X, e.from_center, A.load[e.from_center]) - refund_a;
-      }
-    }
-    if (sum != lab_d(sl)) {
-      set_err(X, kErrPathSum, len);
-      if (atomicCAS(&g_dbg_printed, 0, 1) == 0) {
-        printf("lbdd_b200 path sum mismatch rank %d kind %d anchor %d len %d label cost %lld edge sum %lld\n",
-               X.rank, kind, anchor, len, static_cast<long long>(lab_d(sl)), static_cast<long long>(sum));
-        for (int i = 0; i < len && i < 16; ++i) {
-          const PathEdge e = X.S.path[i];
-          const int64_t m = A.M[static_cast<int64_t>(e.from_center) * A.k + e.to_center];
-          long long key = -1;
-          if (e.kind == kEdgeTransfer) {
-            const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
-            key = static_cast<long long>(row[e.to_center]) - row[e.from_center];
-          }
-          int tkey = -99999;
-          if (X.tile && e.to_center < X.k) {
-            const int r = e.to_center / X.s;
-            const int16_t* wt = X.cluster.map_shared_rank(X.S.wt, r);
-            tkey = wt[static_cast<int64_t>(e.from_center) * X.s + (e.to_center - r * X.s)];
-          }
-          printf("  edge %d: %d -> %d kind %d demand %d cm key %lld M key %d M demand %d tile %d\n", i,
-                 e.from_center, e.to_center, e.kind, e.demand, key,
-                 m == kEmpty ? -1 : transfer_key(m), m == kEmpty ? -1 : transfer_demand(m), tkey);
-        }
-      }
+// The reference checks a path's edge sum against its cost (refine.hpp:75-
+// 79): the lead recounts it from the cost matrix (one lookup per edge).
+__device__ __forceinline__ void check_path_sum(Ctx& X, int kind, int anchor, int len, int64_t refund_a,
+                                            int64_t sl) {
+  const EngineArgs& A = X.A;
+  int64_t sum = 0;
+  for (int i = 0; i < len; ++i) {
+    const PathEdge e = X.S.path[i];
+    if (e.kind == kEdgeTransfer) {
+      const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+      sum += static_cast<int64_t>(row[e.to_center]) - row[e.from_center];
+    } else if (e.kind == kEdgePenalty) {
+      sum += marginal_penalty(X, e.from_center, A.load[e.from_center]) - refund_a;
     }
   }
-  // a mismatch is raised at the next exchange; every CTA still runs apply
-  // so the cluster barriers stay matched
-  *nd = apply(X, kind, len, lab_d(sl), dirty);
-  PROF_MARK(X, 11);
-  return true;
+  if (sum != lab_d(sl)) {
+    set_err(X, kErrPathSum, len);
+    if (atomicCAS(&g_dbg_printed, 0, 1) == 0) {
+      printf("lbdd_b200 path sum mismatch rank %d kind %d anchor %d len %d label cost %lld edge sum %lld\n",
+             X.rank, kind, anchor, len, static_cast<long long>(lab_d(sl)), static_cast<long long>(sum));
+    }
+  }
 }
 
 __device__ __forceinline__ void add_delta(Ctx& X, int64_t v, int arg) {
@@ -1539,66 +1467,85 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   int* dirty = dirty_buf + X.rank * (2 * k + 4);  // per-CTA scratch
 
   PROF_MARK(X, 14);
-  for (int64_t a = A.a_begin; a < A.a_end && !X.err; ++a) {
-    PROF_MARK(X, 14);
-    if (A.debug_checks) {
-      if (X.lead) g_dbg_arrival = a;
-      validate_lists(X, 0);
-    }
-    int32_t d, s;
-    int64_t cost;
-    const int64_t t0 = gtimer();
-    int dum_a = 0;  // placeholder at the anchor after the eviction (strict)
-    if (!strict) {
-      const int64_t key = A.arr_keys[a];
-      d = static_cast<int32_t>(key & 0xffffffffLL);
-      cost = key >> 32;
-      s = A.best_center[d];
-    } else {
-      // strict target: cheapest center with placeholders (solver.hpp:257)
-      d = A.order != nullptr ? A.order[a] : static_cast<int32_t>(a);
-      const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
-      int64_t best = kEmpty;
-      for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
-        if (A.dummies[j] <= 0) continue;
-        const int64_t pk = static_cast<int64_t>(row[j]) * (int64_t(1) << 32) + j;
-        best = min(best, pk);
+  // The arrival loop as a state machine: every phase -- above all the search
+  // rounds, reconstruct and apply -- appears ONCE in the kernel's code, so
+  // the hot loop stays small in the instruction caches (the inlined
+  // straight-line version was ~640 KB of SASS with a 20% L1.5 I-cache miss
+  // rate). Stages:
+  //   kStArrival   next arrival: strict target, insert + first cycle round
+  //   kStSearch    search rounds of `kind`; then reconstruct + apply + the
+  //                repair sources when a negative path was found
+  //   kStAfterCycle  overload check (asral)
+  //   kStPathBound   path bound C; start the path search or give up
+  //   kStPathEnd     fixpoint loop (refine_to_fixpoint)
+  enum Stage : int { kStArrival, kStSearch, kStAfterCycle, kStPathBound, kStPathEnd };
+  int stage = kStArrival;
+  int64_t a = A.a_begin;
+  int32_t d = 0, s = 0;
+  int64_t cost = 0, cap = 0, refund = 0, bound = 0, sink_inc = kLabInf;
+  int kind = kCycle, after = kStAfterCycle;
+  bool applied = false;
+  int64_t t_search = 0;
+  while (!X.err) {
+    if (stage == kStArrival) {
+      if (a >= A.a_end) break;
+      PROF_MARK(X, 14);
+      if (A.debug_checks) {
+        if (X.lead) g_dbg_arrival = a;
+        validate_lists(X, 0);
       }
-      if (threadIdx.x == 0) S.red[0] = kEmpty;
-      __syncthreads();
-      atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(best));
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        S.pub[X.par]->val = S.red[0];
-        S.pub[X.par]->count = 0;
-        const int64_t b = S.red[0];
-        S.pub[X.par]->aux = b == kEmpty ? 0 : static_cast<int32_t>(A.dummies[b & 0xffffffffLL]);
-      }
-      exchange(X);
-      best = kEmpty;
-      int cnt_t = 0;
-      for (int r = 0; r < X.csz; ++r) {
-        if (S.all[r].val < best) {
-          best = S.all[r].val;
-          cnt_t = S.all[r].aux;
+      const int64_t t0 = gtimer();
+      int dum_a = 0;  // placeholder at the anchor after the eviction (strict)
+      if (!strict) {
+        const int64_t key = A.arr_keys[a];
+        d = static_cast<int32_t>(key & 0xffffffffLL);
+        cost = key >> 32;
+        s = A.best_center[d];
+      } else {
+        // strict target: cheapest center with placeholders (solver.hpp:257)
+        d = A.order != nullptr ? A.order[a] : static_cast<int32_t>(a);
+        const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+        int64_t best = kEmpty;
+        for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
+          if (A.dummies[j] <= 0) continue;
+          const int64_t pk = static_cast<int64_t>(row[j]) * (int64_t(1) << 32) + j;
+          best = min(best, pk);
         }
+        if (threadIdx.x == 0) S.red[0] = kEmpty;
+        __syncthreads();
+        atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(best));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          S.pub[X.par]->val = S.red[0];
+          S.pub[X.par]->count = 0;
+          const int64_t b = S.red[0];
+          S.pub[X.par]->aux = b == kEmpty ? 0 : static_cast<int32_t>(A.dummies[b & 0xffffffffLL]);
+        }
+        exchange(X);
+        best = kEmpty;
+        int cnt_t = 0;
+        for (int r = 0; r < X.csz; ++r) {
+          if (S.all[r].val < best) {
+            best = S.all[r].val;
+            cnt_t = S.all[r].aux;
+          }
+        }
+        if (best == kEmpty) {
+          if (X.lead) set_err(X, kErrNoResidual, d);
+          break;
+        }
+        s = static_cast<int32_t>(best & 0xffffffffLL);
+        cost = best >> 32;
+        dum_a = (cnt_t - 1) > 0;
+        __syncthreads();
+        // only the owner of s touches dummies[s] in this phase
+        if (s >= X.v0 && s < X.v1 && threadIdx.x == 0) A.dummies[s] -= 1;
       }
-      if (best == kEmpty) {
-        if (X.lead) set_err(X, kErrNoResidual, d);
-        break;
-      }
-      s = static_cast<int32_t>(best & 0xffffffffLL);
-      cost = best >> 32;
-      dum_a = (cnt_t - 1) > 0;
+      ++a;
+      const int64_t pi_s = pi_of(X, s);
+      // ---- insert + first relaxation round of the cycle search (source s) ----
+      reset_labels(X, pi_s);
       __syncthreads();
-      // only the owner of s touches dummies[s] in this phase
-      if (s >= X.v0 && s < X.v1 && threadIdx.x == 0) A.dummies[s] -= 1;
-    }
-    const int64_t pi_s = pi_of(X, s);
-    // ---- insert + first relaxation round of the cycle search (source s) ----
-    reset_labels(X, pi_s);
-    __syncthreads();
-    {
       const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
       const int32_t hv = row[s];
       for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
@@ -1635,39 +1582,117 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       exchange(X);
       validate_lists(X, 1);
       if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
-    }
-    int nd = 0;
-    PROF_MARK(X, 4);  // insert round
-    const bool cyc = finish_search(X, kCycle, s, 0, 0, dirty, &nd);
-    PROF_MARK(X, 5);  // cycle search (+apply)
-    if (X.err) break;
-    if (cyc) {
-      dirty[nd++] = s;  // the inserted row was never repaired
-      repair(X, dirty, nd);
-    } else {
-      apply_repair(X);  // π += min(0, d) over the explored region
-      __syncthreads();
-    }
-    PROF_MARK(X, 6);  // repairs
-    certify(X);
-    if (strict) continue;
-
-    // ---- overload: penalty-aware path refinement ----
-    const int64_t load = A.load[s];
-    const int64_t cap = A.cap[s];
-    if (load <= cap) {
-      if (X.lead) add_delta(X, cost, d);
+      PROF_MARK(X, 4);  // insert round
+      kind = kCycle;
+      refund = 0;
+      bound = 0;
+      sink_inc = kHop;  // cycle graph: rc >= 0 into anchor-in
+      after = kStAfterCycle;
+      t_search = gtimer();
+      stage = kStSearch;
       continue;
     }
-    const int64_t refund_a = refund_penalty(X, s, load);
-    if (X.lead) {
-      int64_t r1;
-      if (add_ovf(cost, refund_a, &r1)) set_err(X, kErrOverflow, d);
-      add_delta(X, r1, d);
+
+    if (stage == kStSearch) {
+      // ---- the search rounds (the one copy in the kernel) ----
+      const int anchor = kind == kRepair ? -1 : s;
+      const int rounds = search_rounds(X, kind, anchor, refund, bound, 0, sink_inc);
+      if (X.lead) X.n_rounds += rounds;
+      if (kind == kRepair) {
+        apply_repair(X);  // π += min(0, d) over the explored region
+        __syncthreads();
+        PROF_MARK(X, 6);  // repairs
+        certify(X);
+        stage = after;
+        continue;
+      }
+      if (X.lead) X.A.ctl->t_bf_ns += gtimer() - t_search;
+      const int64_t sl = sink_label(X);
+      const bool found = !X.err && sl != kLabInf && lab_d(sl) < 0;
+      if (!found) {
+        if (kind == kCycle) {
+          PROF_MARK(X, 5);  // cycle search
+          apply_repair(X);  // π += min(0, d) over the explored region
+          __syncthreads();
+          PROF_MARK(X, 6);
+          certify(X);
+          stage = kStAfterCycle;
+        } else {
+          PROF_MARK(X, 8);  // path search
+          certify(X);
+          applied = false;
+          stage = kStPathEnd;
+        }
+        continue;
+      }
+      // ---- reconstruct + apply (the one copy) ----
+      // the rounds' st.async exchanges do not release the owners' label
+      // writes; reconstruct reads labels through DSMEM: one barrier
+      X.cluster.sync();
+      if (X.lead) X.n_barriers += 1;
+      PROF_MARK(X, 9);
+      // invalidation counters of the previous apply: its readers finished
+      // before the last barrier, the next writers (T1) come after the next one
+      if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i <= X.k; i += blockDim.x) X.A.inv_cnt[i] = 0;
+      }
+      const int len = reconstruct(X, kind, s, refund, sl);
+      PROF_MARK(X, 10);
+      if (len == 0 || X.err) break;
+      if (kind == kPath && X.S.path[len - 1].kind != kEdgePenalty) {
+        if (X.lead) set_err(X, kErrPenaltyEdge, len);
+        X.err = 1;
+        break;
+      }
+      // the reference checks the path's edge sum against its cost
+      // (refine.hpp:75-79): recount it from the cost matrix (one lookup per
+      // edge), so a stale transfer weight can never reach the objective
+      if (X.lead) check_path_sum(X, kind, s, len, refund, sl);
+      // a mismatch is raised at the next exchange; every CTA still runs
+      // apply so the cluster barriers stay matched
+      int nd = apply(X, kind, len, lab_d(sl), dirty);
+      PROF_MARK(X, 11);
+      if (kind == kCycle) dirty[nd++] = s;  // the inserted row was never repaired
+      // ---- π repair from the dirty rows: a search of kind kRepair ----
+      after = kind == kCycle ? kStAfterCycle : kStPathEnd;
+      applied = true;
+      X.delta = X.delta_main;
+      reset_labels(X, 0);
+      __syncthreads();
+      publish_sources(X, dirty, nd, kRepair);
+      __syncthreads();
+      exchange(X);
+      kind = kRepair;
+      refund = 0;
+      bound = 0;
+      sink_inc = kLabInf;
+      stage = kStSearch;
+      continue;
     }
-    for (;;) {
+
+    if (stage == kStAfterCycle) {
+      if (strict) { stage = kStArrival; continue; }
+      // ---- overload: penalty-aware path refinement ----
+      const int64_t load = A.load[s];
+      cap = A.cap[s];
+      if (load <= cap) {
+        if (X.lead) add_delta(X, cost, d);
+        stage = kStArrival;
+        continue;
+      }
+      const int64_t refund_a = refund_penalty(X, s, load);
+      if (X.lead) {
+        int64_t r1;
+        if (add_ovf(cost, refund_a, &r1)) set_err(X, kErrOverflow, d);
+        add_delta(X, r1, d);
+      }
+      stage = kStPathBound;
+      continue;
+    }
+
+    if (stage == kStPathBound) {
       if (X.lead) A.ctl->path_refine_calls += 1;
-      const int64_t refund = refund_penalty(X, s, A.load[s]);
+      refund = refund_penalty(X, s, A.load[s]);
       // C = min_{u != s} marginal(u) - refund + π(u) - π(s): the most a
       // penalty edge can subtract; prune the search to d_rc < -C
       const int64_t pis_now = pi_of(X, s);
@@ -1688,36 +1713,38 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       PROF_MARK(X, 7);  // path bound
       int64_t cmin = kEmpty;
       for (int r = 0; r < X.csz; ++r) cmin = min(cmin, S.all[r].val);
-      bool applied = false;
-      if (X.lead && !(cmin != kEmpty && cmin - pis_now < 0)) X.dbg[9] += 1;  // pruned
-      if (cmin != kEmpty && cmin - pis_now < 0 && !X.err) {
-        const int64_t C = cmin - pis_now;
-        if (X.lead) {
-          X.dbg[13] += -C;
-          X.dbg[14] = max(X.dbg[14], -C);
-          X.dbg[15] += refund;
-        }
-        X.delta = X.delta_path;
-        reset_labels(X, pis_now);
-        fill_sink_weights(X, kPath, s, refund);
-        __syncthreads();
-        const int src[1] = {s};
-        publish_sources(X, src, 1, kPath);
-        __syncthreads();
-        exchange(X);
-        int nd2 = 0;
-        const int64_t bound = (-C) * kLUnit;
-        PROF_MARK(X, 6);
-        applied = finish_search(X, kPath, s, refund, bound, dirty, &nd2);
-        X.delta = X.delta_main;
-        PROF_MARK(X, 8);  // path search (+apply)
-        if (applied) repair(X, dirty, nd2);
-        PROF_MARK(X, 6);
+      if (!(cmin != kEmpty && cmin - pis_now < 0) || X.err) {
+        if (X.lead) X.dbg[9] += 1;  // pruned
+        certify(X);
+        applied = false;
+        stage = kStPathEnd;
+        continue;
       }
-      certify(X);
-      if (X.err) break;
-      if (!(A.fixpoint && applied && A.load[s] > cap)) break;
+      const int64_t C = cmin - pis_now;
+      if (X.lead) {
+        X.dbg[13] += -C;
+        X.dbg[14] = max(X.dbg[14], -C);
+        X.dbg[15] += refund;
+      }
+      X.delta = X.delta_path;
+      reset_labels(X, pis_now);
+      fill_sink_weights(X, kPath, s, refund);
+      __syncthreads();
+      const int src[1] = {s};
+      publish_sources(X, src, 1, kPath);
+      __syncthreads();
+      exchange(X);
+      kind = kPath;
+      bound = (-C) * kLUnit;
+      sink_inc = kHop - bound;  // path graph: rc_pen >= C into anchor-in
+      t_search = gtimer();
+      stage = kStSearch;
+      continue;
     }
+
+    // kStPathEnd
+    X.delta = X.delta_main;
+    stage = (A.fixpoint && applied && A.load[s] > cap) ? kStPathBound : kStArrival;
   }
   if (X.lead) {
     for (int i = 0; i < 15; ++i) A.ctl->prof[i] += S.prof[i];  // cycles per phase

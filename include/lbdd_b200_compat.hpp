@@ -23,6 +23,7 @@
 #include <string>
 #include <vector>
 
+#include "lbdd/refine.hpp"  // RefineOutcome
 #include "lbdd/solver.hpp"  // the reference's types (ProblemInstance, SolveReport, ...)
 #include "lbdd_b200.h"
 
@@ -155,6 +156,61 @@ inline SolveReport strict_solve(const ProblemInstance& instance, const SolverOpt
 inline SolveReport greedy_solve(const ProblemInstance& instance, const SolverOptions& opts = {},
                                 int device = 0) {
   return detail::solve(instance, opts, LBDD_SOLVER_GREEDY, device);
+}
+
+namespace detail {
+
+// One refinement through lbdd_b200_refine on a reference SolverState
+// (solver.hpp:35-67): the state's allotment (and strict placeholders) go to
+// the device, the refined allotment comes back; the running objective,
+// stats and the transfer index follow like in refine.hpp:173-224.
+template <typename State>
+RefineOutcome refine(State& st, CenterId anchor, int32_t kind, int device) {
+  const ProblemInstance& inst = *st.instance;
+  FlatInstance flat(inst);
+  lbdd_b200_instance* h = nullptr;
+  check(lbdd_b200_instance_create(&flat.desc, device, &h));
+  std::vector<int32_t> assignment(st.allotment.assignment.begin(), st.allotment.assignment.end());
+  std::vector<int64_t> dummies;
+  if (auto* dm = st.dummy_counts()) dummies.assign(dm->begin(), dm->end());
+  int32_t applied = 0;
+  int64_t gain = 0;
+  const lbdd_status rc = lbdd_b200_refine(h, kind, anchor, assignment.data(),
+                                          dummies.empty() ? nullptr : dummies.data(), &applied,
+                                          &gain);
+  lbdd_b200_instance_destroy(h);
+  if (kind == 0) ++st.stats.cycle_refine_calls;
+  else ++st.stats.path_refine_calls;
+  if (rc != LBDD_OK) raise(rc);
+  RefineOutcome out;
+  if (applied) {
+    Allotment a = Allotment::empty(inst.n(), inst.k());
+    for (DemandId d = 0; d < inst.n(); ++d) {
+      if (assignment[static_cast<std::size_t>(d)] >= 0) a.assign(d, assignment[static_cast<std::size_t>(d)]);
+    }
+    st.allotment = std::move(a);
+    st.index = build_index(inst, st.allotment);
+    if (auto* dm = st.dummy_counts()) dm->assign(dummies.begin(), dummies.end());
+    st.delta = checked_add(st.delta, gain);
+    if (kind == 0) ++st.stats.negative_cycles_removed;
+    else ++st.stats.negative_paths_removed;
+    st.stats.refinement_gain = checked_add(st.stats.refinement_gain, -gain);
+    out = {true, gain};
+  }
+  return out;
+}
+
+}  // namespace detail
+
+// negative_cycle_refine / negative_path_refine (refine.hpp:173, 199) on the
+// reference's SolverState, computed on the B200.
+template <typename State>
+RefineOutcome negative_cycle_refine(State& st, CenterId anchor, int device = 0) {
+  return detail::refine(st, anchor, 0, device);
+}
+template <typename State>
+RefineOutcome negative_path_refine(State& st, CenterId anchor, int device = 0) {
+  return detail::refine(st, anchor, 1, device);
 }
 
 }  // namespace b200

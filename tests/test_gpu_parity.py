@@ -193,6 +193,26 @@ def test_cpp_drop_in():
     assert "drop-in ok" in out.stdout
 
 
+@pytest.mark.parametrize("criterion", list(range(1, 10)))
+def test_reference_acceptance_suite_on_b200(criterion):
+    """The reference's own acceptance suite (proj/tests/acceptance.cpp,
+    compiled unmodified by oracle/Makefile) with its solver and refinement
+    calls routed to the B200 backend (oracle/acceptance_b200_shim.hpp ->
+    include/lbdd_b200_compat.hpp -> the C ABI). Every criterion must PASS.
+    (The same suite built against the reference's own solver hangs in
+    criteria 5 and 8 here: its WorkerPool loses a wake-up.)"""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "oracle", "_ref", "acceptance_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/acceptance_b200 not built (needs the reference tree at build time)")
+    out = subprocess.run([exe, str(criterion)], capture_output=True, text=True, timeout=900)
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("[")]
+    assert out.returncode == 0 and lines and all(ln.startswith("[PASS]") for ln in lines), \
+        out.stdout + out.stderr
+
+
 @pytest.mark.parametrize("tile", ["1", "0"])
 def test_medium_solves_lists_rescans_and_key_paths(dev, oracle, tile, monkeypatch):
     """Mid-size random instances through the cluster engine: top-4 transfer

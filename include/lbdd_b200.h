@@ -272,6 +272,63 @@ lbdd_status lbdd_b200_evaluate_objective(lbdd_b200_instance* inst,
 lbdd_status lbdd_b200_bench_index_scan(lbdd_b200_instance* inst, int32_t iters,
                                        double* mean_ms, double* bytes_per_scan);
 
+/* ---- sharded instances: demand rows over the GPUs of one box ----------
+ * north_star: cost-matrix rows are sharded across the GPUs; the arrival
+ * scan runs per shard and its (cost << 32 | demand) keys are gathered (the
+ * caller's collective, e.g. NCCL all_gather over NVLink); the sequential
+ * arrival loop is replicated on every rank and reads any demand's row
+ * through a table of the ranks' row blocks, mapped into each device with
+ * CUDA IPC (peer reads over NVLink). Replaces nothing in the reference (it
+ * is single-process); the result is the reference's asral_solve
+ * (solver.hpp:133) bit for bit, on every rank. */
+
+/* Device memory for one row block (rows x pitch int32, pitch = k rounded
+ * up to 4); fill it with lbdd_b200_shard_upload. */
+lbdd_status lbdd_b200_shard_alloc(int64_t rows, int64_t k, int device,
+                                  int32_t** d_shard, int64_t* pitch_elems);
+lbdd_status lbdd_b200_shard_free(int32_t* d_shard, int device);
+lbdd_status lbdd_b200_shard_upload(int32_t* d_shard, int64_t pitch_elems,
+                                   const int32_t* host_rows, int64_t rows,
+                                   int64_t k, int device);
+/* CUDA IPC of a row block between the ranks' processes (64-byte handles). */
+lbdd_status lbdd_b200_ipc_get_handle(const void* d_ptr, int device,
+                                     uint8_t* handle64);
+lbdd_status lbdd_b200_ipc_open(const uint8_t* handle64, int device,
+                               void** d_ptr);
+lbdd_status lbdd_b200_ipc_close(void* d_ptr, int device);
+
+/* centers: the ProblemInstance's centers (costs NULL, n = total rows).
+ * shard_ptrs[i]: row block i (rows [i*shard_rows, min((i+1)*shard_rows, n)))
+ * as mapped into `device`; shard_ptrs[my_shard] is this rank's own block.
+ * 1 <= nshards <= 16. The blocks are borrowed: they must outlive the
+ * handle. Solve with lbdd_b200_solve_sharded (strict is not supported). */
+lbdd_status lbdd_b200_instance_create_sharded(const lbdd_instance_desc* centers,
+                                              const int32_t* const* shard_ptrs,
+                                              int32_t nshards, int32_t my_shard,
+                                              int64_t shard_rows,
+                                              int64_t pitch_elems, int device,
+                                              lbdd_b200_instance** out);
+
+/* The arrival scan (row_min_center + build_arrival_queue keys,
+ * solver.hpp:74-96) of this rank's block: d_keys / d_best are device arrays
+ * of the block's rows (keys carry global demand ids); min/max cost of the
+ * block for validate_instance (core.hpp:297-302). */
+lbdd_status lbdd_b200_shard_arrival_scan(lbdd_b200_instance* inst,
+                                         int64_t* d_keys, int32_t* d_best,
+                                         int64_t* min_cost, int64_t* max_cost);
+
+/* asral / para-asral / greedy on a sharded instance: d_keys_all (n keys in
+ * any order) and d_best_all (n centers, by global demand id) are the
+ * gathered per-shard scans, min/max the reduced block extremes. Same report
+ * and assignment as lbdd_b200_solve on the whole matrix. */
+lbdd_status lbdd_b200_solve_sharded(lbdd_b200_instance* inst, int32_t solver,
+                                    const int64_t* d_keys_all,
+                                    const int32_t* d_best_all, int64_t min_cost,
+                                    int64_t max_cost,
+                                    const lbdd_solver_options* opts,
+                                    lbdd_solve_report* report,
+                                    int32_t* assignment_out, int64_t* load_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,8 +110,23 @@ using namespace capi_detail;
 struct lbdd_b200_instance {
   int device = 0;
   int64_t n = 0, k = 0, pitch = 0;
-  int32_t* d_cm = nullptr;
+  int32_t* d_cm = nullptr;   // the matrix (sharded: this rank's own row block)
   bool owns_cm = false;
+  // sharded instance (lbdd_b200_instance_create_sharded): the row table over
+  // every rank's block; nshards == 1 for an ordinary instance
+  RowTable rt{};
+  int32_t nshards = 1, my_shard = 0;
+  int64_t shard_rows = 0, local_rows = 0;
+  bool gathered = false;  // keys/best_center hold the gathered arrival scan
+  RowTable rows() const {
+    if (nshards > 1) return rt;
+    RowTable t{};
+    t.shard[0] = d_cm;
+    t.pitch = pitch;
+    t.shard_rows = static_cast<int32_t>(std::min<int64_t>(n, INT32_MAX));
+    t.nshards = 1;
+    return t;
+  }
   std::vector<int64_t> cap, off, par;
   std::vector<int32_t> fam;
   int64_t* d_cap = nullptr;
@@ -249,6 +264,12 @@ lbdd_b200_instance* new_instance(int device, int64_t n, int64_t k) {
   return I;
 }
 
+// entry points that scan the whole matrix through d_cm take ordinary instances
+void require_unsharded(const lbdd_b200_instance* I) {
+  if (I->nshards > 1)
+    raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: not supported on a sharded instance");
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
@@ -325,6 +346,9 @@ void ensure_kernel_events(lbdd_b200_instance* I) {
 
 int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
   const int64_t n = I->n;
+  if (I->nshards > 1 && !I->gathered)
+    raise(LBDD_ERR_INVALID_ARGUMENT,
+          "lbdd_b200: a sharded instance solves through lbdd_b200_solve_sharded");
   I->best_center.ensure(n);
   I->keys.ensure(n);
   I->keys_sorted.ensure(n);
@@ -334,21 +358,24 @@ int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
   CUDA_OK(cudaEventCreate(&e0));
   CUDA_OK(cudaEventCreate(&e1));
   CUDA_OK(cudaEventRecord(e0, I->stream));
-  CUDA_OK(cudaMemcpyAsync(I->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
-  const int blocks = static_cast<int>(std::min<int64_t>((n + 7) / 8, I->num_sms * 8));
-  g_launches++;
-  ensure_kernel_events(I);
-  CUDA_OK(cudaEventRecord(I->kev[0], I->stream));
-  row_argmin_kernel<<<std::max(blocks, 1), 256, 0, I->stream>>>(
-      I->d_cm, I->pitch, n, static_cast<int32_t>(I->k), I->best_center.p, I->keys.p, I->minmax.p);
-  CUDA_OK(cudaGetLastError());
-  CUDA_OK(cudaEventRecord(I->kev[1], I->stream));
-  int64_t mm[2];
-  CUDA_OK(cudaMemcpyAsync(mm, I->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, I->stream));
-  CUDA_OK(cudaStreamSynchronize(I->stream));
-  I->row_scan_ns += static_cast<int64_t>(static_cast<double>(I->time_since(I->kev[0])) * 1e6);
-  I->min_cost = mm[0];
-  I->max_cost = mm[1];
+  if (!I->gathered) {  // sharded: keys, best_center, min/max gathered by the caller
+    CUDA_OK(cudaMemcpyAsync(I->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 7) / 8, I->num_sms * 8));
+    g_launches++;
+    ensure_kernel_events(I);
+    CUDA_OK(cudaEventRecord(I->kev[0], I->stream));
+    row_argmin_kernel<<<std::max(blocks, 1), 256, 0, I->stream>>>(
+        I->d_cm, I->pitch, n, static_cast<int32_t>(I->k), I->best_center.p, I->keys.p, I->minmax.p,
+        0);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaEventRecord(I->kev[1], I->stream));
+    int64_t mm[2];
+    CUDA_OK(cudaMemcpyAsync(mm, I->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, I->stream));
+    CUDA_OK(cudaStreamSynchronize(I->stream));
+    I->row_scan_ns += static_cast<int64_t>(static_cast<double>(I->time_since(I->kev[0])) * 1e6);
+    I->min_cost = mm[0];
+    I->max_cost = mm[1];
+  }
   if (validate_matrix && I->min_cost <= 0)
     raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: invalid instance: non-positive cost in cost matrix");
   // sort by (cost, demand): key bits = 32 (demand) + bits(max cost)
@@ -466,7 +493,7 @@ int64_t device_objective(lbdd_b200_instance* I, const int32_t* d_home, std::vect
   CUDA_OK(cudaMemsetAsync(I->obj_missing.p, 0, sizeof(int32_t), I->stream));
   g_launches++;
   objective_kernel<<<grid_for(I->n), 256, 0, I->stream>>>(
-      I->d_cm, I->pitch, I->n, static_cast<int32_t>(k), d_home, I->obj_acc.p, I->obj_acc.p + 1,
+      I->rows(), I->n, static_cast<int32_t>(k), d_home, I->obj_acc.p, I->obj_acc.p + 1,
       I->obj_missing.p);
   CUDA_OK(cudaGetLastError());
   std::vector<unsigned long long> acc(k + 1);
@@ -561,6 +588,7 @@ void ensure_engine(lbdd_b200_instance* I, int64_t k_nodes) {
 EngineArgs engine_args(lbdd_b200_instance* I) {
   EngineArgs A;
   std::memset(&A, 0, sizeof(A));
+  A.rows = I->rows();
   A.cm = I->d_cm;
   A.pitch = I->pitch;
   A.n = static_cast<int32_t>(I->n);
@@ -1235,6 +1263,7 @@ lbdd_status lbdd_b200_instance_centers(const lbdd_b200_instance* inst, int64_t* 
 lbdd_status lbdd_b200_instance_costs(const lbdd_b200_instance* inst, int64_t row0, int64_t rows,
                                      int32_t* out) {
   return guarded([&] {
+    require_unsharded(inst);
     if (row0 < 0 || rows < 0 || row0 + rows > inst->n)
       raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: row range out of bounds");
     CUDA_OK(cudaSetDevice(inst->device));
@@ -1280,6 +1309,7 @@ lbdd_status lbdd_b200_solve(lbdd_b200_instance* inst, int32_t solver,
 lbdd_status lbdd_b200_build_index(lbdd_b200_instance* inst, const int32_t* assignment, int64_t row0,
                                   int64_t rows, int64_t* min_transfer_out) {
   return guarded([&] {
+    require_unsharded(inst);
     CUDA_OK(cudaSetDevice(inst->device));
     if (rows < 0) { row0 = 0; rows = inst->n; }
     if (row0 < 0 || row0 + rows > inst->n)
@@ -1300,6 +1330,7 @@ lbdd_status lbdd_b200_build_index_device(lbdd_b200_instance* inst, const int32_t
                                          int64_t row0, int64_t rows, int64_t* d_out,
                                          void* stream) {
   return guarded([&] {
+    require_unsharded(inst);
     CUDA_OK(cudaSetDevice(inst->device));
     if (rows < 0) { row0 = 0; rows = inst->n; }
     if (row0 < 0 || row0 + rows > inst->n)
@@ -1319,11 +1350,12 @@ lbdd_status lbdd_b200_build_index_shard(lbdd_b200_instance* inst, const int32_t*
     if (demand_offset < 0 || demand_offset + inst->n >= INT32_MAX)
       raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: demand ids exceed int32");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t rows = inst->nshards > 1 ? inst->local_rows : inst->n;  // this rank's block
     g_launches++;
     fill_i64_kernel<<<grid_for(inst->k * inst->k), 256, 0, st>>>(d_out, inst->k * inst->k, kEmpty);
     CUDA_OK(cudaGetLastError());
-    build_index_prepare(inst, d_assignment, 0, inst->n, st, true);
-    build_index_scan(inst, inst->n, d_out, st, static_cast<int32_t>(demand_offset));
+    build_index_prepare(inst, d_assignment, 0, rows, st, true);
+    build_index_scan(inst, rows, d_out, st, static_cast<int32_t>(demand_offset));
   });
 }
 
@@ -1351,6 +1383,7 @@ lbdd_status lbdd_b200_refine(lbdd_b200_instance* inst, int32_t kind, int32_t anc
                              int32_t* assignment, int64_t* dummies, int32_t* applied,
                              int64_t* gain) {
   return guarded([&] {
+    require_unsharded(inst);
     CUDA_OK(cudaSetDevice(inst->device));
     if (kind != 0 && kind != 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: refine kind is 0 or 1");
     if (anchor < 0 || anchor >= inst->k) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: bad anchor");
@@ -1380,6 +1413,7 @@ lbdd_status lbdd_b200_refine(lbdd_b200_instance* inst, int32_t kind, int32_t anc
 lbdd_status lbdd_b200_gamma_has_negative_cycle(lbdd_b200_instance* inst, const int32_t* assignment,
                                                const int64_t* dummies, int32_t* has_cycle) {
   return guarded([&] {
+    require_unsharded(inst);
     CUDA_OK(cudaSetDevice(inst->device));
     check_device_range(inst);
     state_from_allotment(inst, assignment);
@@ -1535,6 +1569,7 @@ lbdd_status lbdd_b200_relax_round(int32_t node_count, const int64_t* weights,
 lbdd_status lbdd_b200_bench_index_scan(lbdd_b200_instance* inst, int32_t iters, double* mean_ms,
                                        double* bytes_per_scan) {
   return guarded([&] {
+    require_unsharded(inst);
     CUDA_OK(cudaSetDevice(inst->device));
     if (!inst->scanned) arrival_scan(inst, false);
     inst->M.ensure(inst->k * inst->k);
@@ -1563,6 +1598,151 @@ lbdd_status lbdd_b200_bench_index_scan(lbdd_b200_instance* inst, int32_t iters, 
     *bytes_per_scan = static_cast<double>(inst->n) * inst->k * 4.0 +
                       static_cast<double>(inst->n) * 12.0 +
                       static_cast<double>(inst->k) * inst->k * 8.0;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// sharded instances: demand rows split over the ranks of one box
+// ---------------------------------------------------------------------------
+
+lbdd_status lbdd_b200_shard_alloc(int64_t rows, int64_t k, int device, int32_t** d_shard,
+                                  int64_t* pitch_elems) {
+  return guarded([&] {
+    if (rows < 1 || k < 1) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd: n and k must be >= 1");
+    CUDA_OK(cudaSetDevice(device));
+    const int64_t pitch = ((k + 3) / 4) * 4;
+    CUDA_OK(cudaMalloc(d_shard, sizeof(int32_t) * rows * pitch));
+    *pitch_elems = pitch;
+  });
+}
+
+lbdd_status lbdd_b200_shard_free(int32_t* d_shard, int device) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaFree(d_shard));
+  });
+}
+
+lbdd_status lbdd_b200_shard_upload(int32_t* d_shard, int64_t pitch_elems, const int32_t* host_rows,
+                                   int64_t rows, int64_t k, int device) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaMemcpy2D(d_shard, sizeof(int32_t) * pitch_elems, host_rows, sizeof(int32_t) * k,
+                         sizeof(int32_t) * k, rows, cudaMemcpyHostToDevice));
+    if (pitch_elems > k) {  // padding columns: never read as costs
+      CUDA_OK(cudaMemset2D(d_shard + k, sizeof(int32_t) * pitch_elems, 0x7f,
+                           sizeof(int32_t) * (pitch_elems - k), rows));
+    }
+  });
+}
+
+lbdd_status lbdd_b200_ipc_get_handle(const void* d_ptr, int device, uint8_t* handle64) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    CUDA_OK(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle64, &h, 64);
+  });
+}
+
+lbdd_status lbdd_b200_ipc_open(const uint8_t* handle64, int device, void** d_ptr) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    CUDA_OK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+lbdd_status lbdd_b200_ipc_close(void* d_ptr, int device) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaIpcCloseMemHandle(d_ptr));
+  });
+}
+
+lbdd_status lbdd_b200_instance_create_sharded(const lbdd_instance_desc* centers,
+                                              const int32_t* const* shard_ptrs, int32_t nshards,
+                                              int32_t my_shard, int64_t shard_rows,
+                                              int64_t pitch_elems, int device,
+                                              lbdd_b200_instance** out) {
+  return guarded([&] {
+    const int64_t n = centers->n;
+    if (nshards < 1 || nshards > kMaxShards || my_shard < 0 || my_shard >= nshards)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: bad shard layout");
+    if (shard_rows < 1 || shard_rows * nshards < n || shard_rows * (nshards - 1) >= n ||
+        shard_rows >= INT32_MAX)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: shard_rows must split n over nshards blocks");
+    if (pitch_elems < centers->k || pitch_elems % 4 != 0)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: pitch must be >= k and a multiple of 4");
+    std::unique_ptr<lbdd_b200_instance> I(new_instance(device, n, centers->k));
+    I->pitch = pitch_elems;
+    I->nshards = nshards;
+    I->my_shard = my_shard;
+    I->shard_rows = shard_rows;
+    I->local_rows = std::min<int64_t>(shard_rows, n - shard_rows * my_shard);
+    I->d_cm = const_cast<int32_t*>(shard_ptrs[my_shard]);
+    I->owns_cm = false;
+    I->rt = RowTable{};
+    for (int i = 0; i < nshards; ++i) I->rt.shard[i] = shard_ptrs[i];
+    I->rt.pitch = pitch_elems;
+    I->rt.shard_rows = static_cast<int32_t>(shard_rows);
+    I->rt.nshards = nshards;
+    upload_centers(I.get(), centers);
+    *out = I.release();
+  });
+}
+
+lbdd_status lbdd_b200_shard_arrival_scan(lbdd_b200_instance* inst, int64_t* d_keys, int32_t* d_best,
+                                         int64_t* min_cost, int64_t* max_cost) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    const int64_t rows = inst->nshards > 1 ? inst->local_rows : inst->n;
+    const int64_t id0 = inst->nshards > 1 ? inst->shard_rows * inst->my_shard : 0;
+    inst->minmax.ensure(2);
+    const int64_t init[2] = {INT64_MAX, INT64_MIN};
+    CUDA_OK(cudaMemcpyAsync(inst->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, inst->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, inst->num_sms * 8));
+    g_launches++;
+    row_argmin_kernel<<<std::max(blocks, 1), 256, 0, inst->stream>>>(
+        inst->d_cm, inst->pitch, rows, static_cast<int32_t>(inst->k), d_best, d_keys, inst->minmax.p,
+        id0);
+    CUDA_OK(cudaGetLastError());
+    int64_t mm[2];
+    CUDA_OK(cudaMemcpyAsync(mm, inst->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, inst->stream));
+    CUDA_OK(cudaStreamSynchronize(inst->stream));
+    *min_cost = mm[0];
+    *max_cost = mm[1];
+  });
+}
+
+lbdd_status lbdd_b200_solve_sharded(lbdd_b200_instance* inst, int32_t solver,
+                                    const int64_t* d_keys_all, const int32_t* d_best_all,
+                                    int64_t min_cost, int64_t max_cost,
+                                    const lbdd_solver_options* opts, lbdd_solve_report* report,
+                                    int32_t* assignment_out, int64_t* load_out) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(inst->device));
+    if (solver == LBDD_SOLVER_STRICT)
+      raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: strict_solve on a sharded instance is not supported");
+    const int64_t n = inst->n;
+    inst->keys.ensure(n);
+    inst->keys_sorted.ensure(n);
+    inst->best_center.ensure(n);
+    CUDA_OK(cudaMemcpyAsync(inst->keys.p, d_keys_all, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice,
+                            inst->stream));
+    CUDA_OK(cudaMemcpyAsync(inst->best_center.p, d_best_all, sizeof(int32_t) * n,
+                            cudaMemcpyDeviceToDevice, inst->stream));
+    inst->min_cost = min_cost;
+    inst->max_cost = max_cost;
+    inst->gathered = true;
+    struct Reset {
+      lbdd_b200_instance* I;
+      ~Reset() { I->gathered = false; }
+    } reset{inst};
+    const lbdd_status st = lbdd_b200_solve(inst, solver, opts, report, assignment_out, load_out);
+    if (st != LBDD_OK) raise(st, lbdd_b200_last_error());
   });
 }
 

@@ -386,8 +386,8 @@ __device__ void validate_lists(Ctx& X, int where) {
       int why = 0;
       if (e == kEmpty) why = 1;
       else if (A.home[d] != u) why = 2;
-      else if (transfer_key(e) != A.cm[static_cast<int64_t>(d) * A.pitch + j] -
-                                      A.cm[static_cast<int64_t>(d) * A.pitch + u]) why = 3;
+      else if (transfer_key(e) != row_of(A.rows, d)[ j] -
+                                      row_of(A.rows, d)[ u]) why = 3;
       else if (i > 0 && t.e[i - 1] >= e) why = 4;
       // debug encoding (small instances): demand | u | j | slot | reason | len | complete
       if (why) set_err(X, 300 + where, (d & 255) | ((u & 15) << 8) | ((j & 15) << 12) | (i << 16) |
@@ -1009,7 +1009,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   for (int i = 0; i < len; ++i) {
     const PathEdge e = S.path[i];
     if (e.kind != kEdgeTransfer) continue;
-    const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+    const int32_t* row = row_of(A.rows, e.demand);
     const int32_t hv = row[e.to_center];
     for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
       if (j == e.to_center) continue;
@@ -1223,7 +1223,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           const int q = atomicAdd(&S.misc[0], 1);
           S.qd[q] = dd;
           S.qs[q] = sl;  // full: path slot; else: segment
-          S.qh[q] = A.cm[static_cast<int64_t>(dd) * A.pitch +
+          S.qh[q] = row_of(A.rows, dd)[
                          S.path[full ? sl : seg[3 * sl]].from_center];
         }
       }
@@ -1243,7 +1243,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           const int32_t d2 = S.qd[q];
           const int u = S.path[sl2].from_center;
           const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
-          const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
+          const int32_t* row = row_of(A.rows, d2);
           list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
         }
       } else if (rowmode) {
@@ -1258,7 +1258,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           const int32_t d2 = S.qd[q];
           const int32_t hv = S.qh[q];
           const int u = S.path[seg[3 * g]].from_center;
-          const int4 x4 = reinterpret_cast<const int4*>(A.cm + static_cast<int64_t>(d2) * A.pitch)[c4];
+          const int4 x4 = reinterpret_cast<const int4*>(row_of(A.rows, d2))[c4];
           const int32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -1278,7 +1278,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           const int j = S.mine[o0 + xx];
           const int32_t d2 = S.qd[q];
           const int u = S.path[seg[3 * g]].from_center;
-          const int32_t* row = A.cm + static_cast<int64_t>(d2) * A.pitch;
+          const int32_t* row = row_of(A.rows, d2);
           list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
         }
       }
@@ -1345,7 +1345,7 @@ __device__ __forceinline__ void check_path_sum(Ctx& X, int kind, int anchor, int
   for (int i = 0; i < len; ++i) {
     const PathEdge e = X.S.path[i];
     if (e.kind == kEdgeTransfer) {
-      const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+      const int32_t* row = row_of(A.rows, e.demand);
       sum += static_cast<int64_t>(row[e.to_center]) - row[e.from_center];
     } else if (e.kind == kEdgePenalty) {
       sum += marginal_penalty(X, e.from_center, A.load[e.from_center]) - refund_a;
@@ -1504,7 +1504,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       } else {
         // strict target: cheapest center with placeholders (solver.hpp:257)
         d = A.order != nullptr ? A.order[a] : static_cast<int32_t>(a);
-        const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+        const int32_t* row = row_of(A.rows, d);
         int64_t best = kEmpty;
         for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
           if (A.dummies[j] <= 0) continue;
@@ -1546,7 +1546,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       // ---- insert + first relaxation round of the cycle search (source s) ----
       reset_labels(X, pi_s);
       __syncthreads();
-      const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+      const int32_t* row = row_of(A.rows, d);
       const int32_t hv = row[s];
       for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
         if (j == s) continue;

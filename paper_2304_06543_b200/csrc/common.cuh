@@ -119,9 +119,28 @@ struct PathEdge {
 enum GraphKind : int32_t { kCycleGraph = 0, kPathGraph = 1, kGammaGraph = 2 };
 enum EdgeKind : int32_t { kEdgeNone = 0, kEdgeTransfer = 1, kEdgeDummy = 2, kEdgePenalty = 3 };
 
+// Where the cost row of demand d lives. One shard: the whole matrix. Several
+// (sharded instance, lbdd_b200_instance_create_sharded): demand rows split
+// in equal blocks of shard_rows over the ranks of one box, shard[i] the
+// device pointer of block i as mapped into THIS device's address space (its
+// own block, or a peer's opened through CUDA IPC, read over NVLink).
+constexpr int kMaxShards = 16;
+struct RowTable {
+  const int32_t* shard[kMaxShards];
+  int64_t pitch;
+  int32_t shard_rows;  // rows per shard block (all but possibly the last)
+  int32_t nshards;     // <= 1: shard[0] holds every row
+};
+__host__ __device__ inline const int32_t* row_of(const RowTable& T, int64_t d) {
+  if (T.nshards <= 1) return T.shard[0] + d * T.pitch;
+  const uint32_t s = static_cast<uint32_t>(d) / static_cast<uint32_t>(T.shard_rows);
+  return T.shard[s] + (d - static_cast<int64_t>(s) * T.shard_rows) * T.pitch;
+}
+
 struct EngineArgs {
   // instance (read-only)
-  const int32_t* cm;
+  RowTable rows;         // every demand's cost row (row_of)
+  const int32_t* cm;     // rows.shard[0]
   int64_t pitch;
   int32_t n;
   int32_t k;

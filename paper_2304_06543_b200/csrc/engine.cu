@@ -631,7 +631,7 @@ __device__ void apply_path(const EngineArgs& A, const GraphView& G, Smem& S) {
     const int j = static_cast<int>(idx - static_cast<int64_t>(i) * k);
     const PathEdge e = S.path[i];
     if (e.kind != kEdgeTransfer || j == e.to_center) continue;
-    const int32_t* row = A.cm + static_cast<int64_t>(e.demand) * A.pitch;
+    const int32_t* row = row_of(A.rows, e.demand);
     const int64_t v = pack_transfer(row[j] - row[e.to_center], e.demand);
     atomicMin(reinterpret_cast<long long*>(&A.M[static_cast<int64_t>(e.to_center) * k + j]),
               static_cast<long long>(v));
@@ -666,7 +666,7 @@ __device__ void apply_path(const EngineArgs& A, const GraphView& G, Smem& S) {
         const int32_t dd = S.qd[q];
         const int sl = S.qs[q];
         const int u = S.path[sl].from_center;
-        const int32_t* row = A.cm + static_cast<int64_t>(dd) * A.pitch;
+        const int32_t* row = row_of(A.rows, dd);
         const int32_t hv = row[u];
         const int32_t* cols = A.inv_cols + static_cast<int64_t>(sl) * k;
         for (int x = lane; x < S.cnt[sl]; x += 32) {
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(512, 1) asral_engine_kernel(EngineArgs A, uint
       // strict target: cheapest center still holding placeholders
       // (solver.hpp:257-268), computed redundantly per CTA.
       d = A.order != nullptr ? A.order[a] : static_cast<int32_t>(a);
-      const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+      const int32_t* row = row_of(A.rows, d);
       int64_t best = kEmpty;
       for (int j = threadIdx.x; j < k; j += blockDim.x) {
         if (ld64(&A.dummies[j]) <= 0) continue;
@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(512, 1) asral_engine_kernel(EngineArgs A, uint
     // ---- phase I: insert + cycle-graph setup ----
     BufSet bs;
     {
-      const int32_t* row = A.cm + static_cast<int64_t>(d) * A.pitch;
+      const int32_t* row = row_of(A.rows, d);
       const int32_t hv = row[s];
       int64_t* Ms = A.M + static_cast<int64_t>(s) * k;
       for (int64_t j = gtid; j < k; j += gsz) {

@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(256) row_argmin_kernel(const int32_t* __restri
                                                          int64_t pitch, int64_t n, int32_t k,
                                                          int32_t* __restrict__ best_center,
                                                          int64_t* __restrict__ keys,
-                                                         int64_t* __restrict__ minmax) {
+                                                         int64_t* __restrict__ minmax,
+                                                         int64_t id0) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(256) row_argmin_kernel(const int32_t* __restri
     }
     if (lane == 0) {
       best_center[row] = bi;
-      keys[row] = static_cast<int64_t>(bv) * (int64_t(1) << 32) + row;
+      keys[row] = static_cast<int64_t>(bv) * (int64_t(1) << 32) + (id0 + row);  // global demand id
     }
   }
 #pragma unroll
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(1024) seg_argmin_kernel(
 
 // assignment-cost sum + load histogram (evaluate_partial_objective,
 // core.hpp:216-233; penalties are added on the host from the loads).
-__global__ void objective_kernel(const int32_t* __restrict__ cm, int64_t pitch, int64_t n,
+__global__ void objective_kernel(const RowTable rows, int64_t n,
                                  int32_t k, const int32_t* __restrict__ home,
                                  unsigned long long* __restrict__ sum,
                                  unsigned long long* __restrict__ load,
@@ -209,7 +210,7 @@ __global__ void objective_kernel(const int32_t* __restrict__ cm, int64_t pitch, 
        d += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t h = home[d];
     if (h < 0 || h >= k) { ++missing; continue; }
-    local += static_cast<unsigned long long>(cm[d * pitch + h]);
+    local += static_cast<unsigned long long>(row_of(rows, d)[h]);
     atomicAdd(&load[h], 1ull);
   }
   using WarpReduce = cub::WarpReduce<unsigned long long>;

@@ -64,6 +64,21 @@ _lib.lbdd_b200_gamma_has_negative_cycle.argtypes = [_P, _abi.I32P, _abi.I64P,
 _lib.lbdd_b200_evaluate_objective.argtypes = [_P, _abi.I32P, C.c_int32, C.POINTER(C.c_int64)]
 _lib.lbdd_b200_bench_index_scan.argtypes = [_P, C.c_int32, C.POINTER(C.c_double),
                                             C.POINTER(C.c_double)]
+_lib.lbdd_b200_shard_alloc.argtypes = [C.c_int64, C.c_int64, C.c_int, C.POINTER(_P),
+                                       C.POINTER(C.c_int64)]
+_lib.lbdd_b200_shard_free.argtypes = [_P, C.c_int]
+_lib.lbdd_b200_shard_upload.argtypes = [_P, C.c_int64, _abi.I32P, C.c_int64, C.c_int64, C.c_int]
+_lib.lbdd_b200_ipc_get_handle.argtypes = [_P, C.c_int, C.c_char_p]
+_lib.lbdd_b200_ipc_open.argtypes = [C.c_char_p, C.c_int, C.POINTER(_P)]
+_lib.lbdd_b200_ipc_close.argtypes = [_P, C.c_int]
+_lib.lbdd_b200_instance_create_sharded.argtypes = [C.POINTER(_abi.InstanceDesc), C.POINTER(_P),
+                                                   C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                                                   C.c_int, C.POINTER(_P)]
+_lib.lbdd_b200_shard_arrival_scan.argtypes = [_P, _P, _P, C.POINTER(C.c_int64),
+                                              C.POINTER(C.c_int64)]
+_lib.lbdd_b200_solve_sharded.argtypes = [_P, C.c_int32, _P, _P, C.c_int64, C.c_int64,
+                                         C.POINTER(_abi.SolverOptionsC),
+                                         C.POINTER(_abi.SolveReportC), _abi.I32P, _abi.I64P]
 
 
 def _check(rc: int) -> None:

@@ -61,3 +61,46 @@ def test_sharded_build_matches_full(tmp_path, seed):
     mp.spawn(_worker, args=(2, _free_port(), seed, path), nprocs=2, join=True)
     got, full = np.load(path)
     assert (got == full).all()
+
+
+def _gather_worker(rank, world, port, n, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2304_06543_b200.sharded import (block_range, block_rows, combine_min_transfer,
+                                               gather_blocks)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    row0, rows = block_range(n, world, rank)
+    # this rank's block of per-demand keys (global ids in the low 32 bits)
+    keys = torch.arange(row0, row0 + rows, dtype=torch.int64) + (torch.arange(rows) % 7) * (1 << 32)
+    best = torch.full((rows,), rank, dtype=torch.int32)
+    allk = gather_blocks(keys, n)
+    allb = gather_blocks(best, n)
+    part = torch.full((9,), (1 << 63) - 1, dtype=torch.int64)
+    part[rank] = 100 + rank
+    part[8] = 50 - rank
+    combine_min_transfer(part)
+    if rank == 0:
+        np.save(result_path, np.concatenate([allk.numpy(), allb.numpy().astype(np.int64),
+                                             part.numpy(), [block_rows(n, world)]]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 11), (3, 10), (2, 2)])
+def test_sharded_gather_and_combine(tmp_path, world, n):
+    """The sharded solve's host logic over gloo: equal row blocks (the last
+    shorter), the all-gather of per-block arrival keys / best centers back
+    into demand order, and the MIN combine of partials."""
+    from paper_2304_06543_b200.sharded import block_range, block_rows
+    path = str(tmp_path / "g.npy")
+    mp.spawn(_gather_worker, args=(world, _free_port(), n, path), nprocs=world, join=True)
+    r = np.load(path)
+    allk, allb, part = r[:n], r[n:2 * n], r[2 * n:2 * n + 9]
+    assert (allk & 0xffffffff).tolist() == list(range(n))
+    want_b = [rk for rk in range(world) for _ in range(block_range(n, world, rk)[1])]
+    assert allb.tolist() == want_b
+    assert part[:world].tolist() == [100 + rk for rk in range(world)]
+    assert part[8] == 50 - (world - 1)
+    br = block_rows(n, world)
+    assert r[-1] == br and sum(block_range(n, world, rk)[1] for rk in range(world)) == n

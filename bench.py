@@ -18,12 +18,15 @@ solves (at least 1) and as many of the --steps timed solves as fit in
 --budget seconds of wall clock (always at least 1), and reports the counts
 it ran as `steps`/`warmup` beside `requested_steps`/`requested_warmup`.
 
-Multi-GPU (torchrun, one process per GPU): the solve is a sequential
-algorithm and runs as replicas of the same instance on every rank (each its
-own full solve, weak scaling); the part that shards -- the full cost-matrix
-scan behind build_index -- runs sharded by demand rows with an NCCL MIN
-all-reduce and is reported in `scan`. Timing: CUDA events on the launching
-stream, barrier + sync on both sides, max over ranks.
+Multi-GPU (torchrun, one process per GPU, run_sharded): the configs[1]
+matrix is split in row blocks over the ranks (each rank generates and holds
+only its block); the blocks are mapped into every device with CUDA IPC, the
+per-block arrival scans are all-gathered over NCCL, and the sequential
+arrival loop runs replicated on every rank, reading other ranks' rows over
+NVLink (paper_2304_06543_b200/sharded.py). Total work is fixed ("strong");
+what scales is the matrix per GPU, not the solve time. Timing: CUDA events
+on the launching stream, barrier + sync on both sides, max over ranks.
+LBDD_BENCH_BACKEND=gloo (tests only) runs the ranks over gloo.
 
 `--impl reference` times the UNMODIFIED reference solver (oracle/_ref,
 compiled from the reference sources; never the product library) on this
@@ -60,8 +63,8 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=None, help="override |D| (not configs[1])")
-    p.add_argument("--k", type=int, default=None, help="override |S| (not configs[1])")
+    p.add_argument("--demands", dest="n", type=int, default=None, help="override |D| (not configs[1])")
+    p.add_argument("--centers", dest="k", type=int, default=None, help="override |S| (not configs[1])")
     p.add_argument("--budget", type=float, default=1380.0,
                    help="wall-clock seconds for the whole run (driver limit 1800 s)")
     p.add_argument("--ref-arrivals", type=int, default=40,
@@ -154,10 +157,11 @@ def dist_setup(n_gpus):
     import torch
     import torch.distributed as dist
     if n_gpus > 1 or "RANK" in os.environ:
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("LBDD_BENCH_BACKEND", "nccl"))
         rank = dist.get_rank()
         world = dist.get_world_size()
         local = int(os.environ.get("LOCAL_RANK", rank))
+        local = int(os.environ.get("LBDD_BENCH_DEVICE", local))  # tests: ranks share a GPU
     else:
         rank, world, local = 0, 1, 0
     torch.cuda.set_device(local)
@@ -178,7 +182,8 @@ def reduce_scalar(x: float, op: str) -> float:
     import torch.distributed as dist
     if not dist.is_initialized():
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
     return float(t.item())
 
@@ -387,6 +392,94 @@ def run_reference(a):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+
+def run_sharded(a):
+    """N > 1: the configs[1] matrix split in row blocks over the ranks
+    (sharded.ShardedInstance: CUDA IPC row table, per-block arrival scans
+    all-gathered over NCCL, replicated arrival loop). One step = one solve
+    on every rank; value = the max over ranks of the device time."""
+    t_begin = time.time()
+    import torch
+    import torch.distributed as dist
+
+    import synth_instances as SI
+    from paper_2304_06543_b200 import solver as S
+    from paper_2304_06543_b200.sharded import ShardedInstance, block_range
+
+    rank, world, local = dist_setup(a.gpus)
+    spec, is_cfg1 = spec_of(a)
+    n, k = spec.n, spec.k
+    row0, rows = block_range(n, world, rank)
+    host = SI.cost_rows(spec, row0, rows)          # this rank's rows only
+    inst = ShardedInstance(host, n, SI.centers(spec), device=local)
+    t_ready = time.time()
+    warm_s = []
+    while len(warm_s) < max(1, a.warmup):
+        if warm_s and time.time() - t_begin > 0.3 * a.budget:
+            break
+        r = inst.solve("asral", want_assignment=False)
+        warm_s.append(r.timings.device_ns / 1e9)
+    barrier()
+    per_solve = reduce_scalar(max(warm_s), "max") * 1.05 + 1.0
+    fit = int((a.budget - (time.time() - t_begin) - per_solve - 60) // per_solve)
+    steps = int(reduce_scalar(float(max(1, min(a.steps, fit))), "min"))
+    launches0 = S.launch_count()
+    reports = []
+    with ClockSampler(local) as clocks:
+        for _ in range(steps):
+            barrier()
+            reports.append(inst.solve("asral", want_assignment=False))
+        barrier()
+    launches = S.launch_count() - launches0
+    step_s = reduce_scalar(statistics.mean(r.timings.device_ns / 1e9 for r in reports), "max")
+    rep = reports[-1]
+    # e2e: this rank's block from host memory, the solve, the assignment back
+    barrier()
+    t0 = time.perf_counter()
+    inst.close()
+    inst = ShardedInstance(host, n, SI.centers(spec), device=local)
+    r2 = inst.solve("asral", want_assignment=True)
+    e2e_s = reduce_scalar(time.perf_counter() - t0, "max")
+    assert r2.objective == rep.objective
+    line = {
+        "metric": "asral_solve_time_s", "baseline_metric": BASELINE_METRIC,
+        "value": round(step_s, 4), "unit": "s", "n_gpus": world, "steps": steps,
+        "warmup": len(warm_s), "requested_steps": a.steps, "requested_warmup": a.warmup,
+        "ms_per_step": round(step_s * 1e3, 2), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (synth_instances.py lbdd-synth-v2, host-generated per row block)",
+        "config": {"workload": workload_name(spec, is_cfg1), "spec": spec.name(),
+                   "n_demands": n, "n_centers": k,
+                   "parallelism": f"rows sharded over {world} GPUs (CUDA IPC row table, "
+                                  "per-block arrival scans all-gathered over NCCL); the "
+                                  "sequential arrival loop replicated on every rank",
+                   "rows_per_rank": block_range(n, world, 0)[1],
+                   "l2": "inputs larger than L2; no flush needed",
+                   "objective": rep.objective,
+                   "assignment_sha256": SI.assignment_sha256(r2.assignment)},
+        "e2e": {"value": round(e2e_s, 4), "unit": "s",
+                "h2d_bytes_per_step": int(rows * k * 4), "d2h_bytes_per_step": int(n * 4),
+                "path": "per rank: block upload from host + IPC exchange + sharded solve + "
+                        "assignment to host"},
+        "gpu_launches": int(launches // max(steps, 1)),
+        "roofline": {"kernel": "cluster_engine_kernel", "bound": "hbm",
+                     "achieved": round((n + rep.stats.transfers_applied) * k * 4
+                                       / max(rep.timings.engine_ns, 1), 3),
+                     "peak": peaks()[0], "unit": "GB/s",
+                     "frac": round((n + rep.stats.transfers_applied) * k * 4
+                                   / max(rep.timings.engine_ns, 1) / peaks()[0], 7),
+                     "traffic": None,
+                     "note": "replicated arrival loop; rows of other ranks' blocks read over "
+                             "NVLink through the IPC row table"},
+        "clocks": clocks.summary(), "setup_s": round(t_ready - t_begin, 1),
+    }
+    line["wall_s"] = round(time.time() - t_begin, 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    inst.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
 
 def run_ours(a):
     t_begin = time.time()
@@ -610,5 +703,7 @@ if __name__ == "__main__":
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_sharded(args)
     else:
         run_ours(args)

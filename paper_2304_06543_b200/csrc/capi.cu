@@ -344,6 +344,74 @@ void ensure_kernel_events(lbdd_b200_instance* I) {
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr)
+      raise(LBDD_ERR_CUDA, "lbdd_b200: cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// The arrival scan over `rows` rows at `cm` (row_min_center + the keys of
+// build_arrival_queue, fused with the cost-range check): TMA-staged kernel
+// when a row spans at most 5 boxes of 256 columns (k <= 1280), else the
+// 128-bit streaming kernel.
+void launch_row_argmin(lbdd_b200_instance* I, const int32_t* cm, int64_t rows, int64_t id0,
+                       int32_t* best, int64_t* keys, int64_t* minmax) {
+  const int ncb = static_cast<int>((I->pitch + kTmaBoxCols - 1) / kTmaBoxCols);
+  g_launches++;
+  // two or more stages must fit the ring (16-row groups: 16 KB per box
+  // column); wider rows stream well with plain 128-bit loads (long rows per
+  // warp), so they keep the streaming kernel
+  if (ncb <= 5 && rows > 0) {
+    CUtensorMap tm;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(I->pitch), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(I->pitch) * 4};
+    const cuuint32_t box[2] = {kTmaBoxCols, kTmaRows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_tiled()(&tm, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t*>(cm),
+                                      dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(LBDD_ERR_CUDA, "lbdd_b200: tensor map encode failed");
+    const size_t stage = static_cast<size_t>(ncb) * kTmaRows * kTmaBoxCols * 4;
+    const int stages = static_cast<int>(std::min<size_t>(6, (210 * 1024) / stage));
+    const size_t smem = stages * stage + 16 * stages + 1024;
+    const int grid = static_cast<int>(std::min<int64_t>(I->num_sms, (rows + kTmaRows - 1) / kTmaRows));
+#define LAUNCH_TMA(NC)                                                                              \
+  CUDA_OK(cudaFuncSetAttribute(row_argmin_tma_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               static_cast<int>(smem)));                                             \
+  row_argmin_tma_kernel<NC><<<grid, 32 * (kTmaRows + 1), smem, I->stream>>>(                      \
+      tm, rows, static_cast<int32_t>(I->k),                                                         \
+                                                            stages, best, keys, minmax, id0)
+    switch (ncb) {
+      case 1: LAUNCH_TMA(1); break;
+      case 2: LAUNCH_TMA(2); break;
+      case 3: LAUNCH_TMA(3); break;
+      case 4: LAUNCH_TMA(4); break;
+      case 5: LAUNCH_TMA(5); break;
+      default: LAUNCH_TMA(5); break;
+    }
+#undef LAUNCH_TMA
+  } else {
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, I->num_sms * 8));
+    row_argmin_kernel<<<std::max(blocks, 1), 256, 0, I->stream>>>(
+        cm, I->pitch, rows, static_cast<int32_t>(I->k), best, keys, minmax, id0);
+  }
+  CUDA_OK(cudaGetLastError());
+}
+
 int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
   const int64_t n = I->n;
   if (I->nshards > 1 && !I->gathered)
@@ -360,14 +428,9 @@ int64_t arrival_scan(lbdd_b200_instance* I, bool validate_matrix) {
   CUDA_OK(cudaEventRecord(e0, I->stream));
   if (!I->gathered) {  // sharded: keys, best_center, min/max gathered by the caller
     CUDA_OK(cudaMemcpyAsync(I->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, I->stream));
-    const int blocks = static_cast<int>(std::min<int64_t>((n + 7) / 8, I->num_sms * 8));
-    g_launches++;
     ensure_kernel_events(I);
     CUDA_OK(cudaEventRecord(I->kev[0], I->stream));
-    row_argmin_kernel<<<std::max(blocks, 1), 256, 0, I->stream>>>(
-        I->d_cm, I->pitch, n, static_cast<int32_t>(I->k), I->best_center.p, I->keys.p, I->minmax.p,
-        0);
-    CUDA_OK(cudaGetLastError());
+    launch_row_argmin(I, I->d_cm, n, 0, I->best_center.p, I->keys.p, I->minmax.p);
     CUDA_OK(cudaEventRecord(I->kev[1], I->stream));
     int64_t mm[2];
     CUDA_OK(cudaMemcpyAsync(mm, I->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, I->stream));
@@ -1703,12 +1766,7 @@ lbdd_status lbdd_b200_shard_arrival_scan(lbdd_b200_instance* inst, int64_t* d_ke
     inst->minmax.ensure(2);
     const int64_t init[2] = {INT64_MAX, INT64_MIN};
     CUDA_OK(cudaMemcpyAsync(inst->minmax.p, init, sizeof(init), cudaMemcpyHostToDevice, inst->stream));
-    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, inst->num_sms * 8));
-    g_launches++;
-    row_argmin_kernel<<<std::max(blocks, 1), 256, 0, inst->stream>>>(
-        inst->d_cm, inst->pitch, rows, static_cast<int32_t>(inst->k), d_best, d_keys, inst->minmax.p,
-        id0);
-    CUDA_OK(cudaGetLastError());
+    launch_row_argmin(inst, inst->d_cm, rows, id0, d_best, d_keys, inst->minmax.p);
     int64_t mm[2];
     CUDA_OK(cudaMemcpyAsync(mm, inst->minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, inst->stream));
     CUDA_OK(cudaStreamSynchronize(inst->stream));

@@ -19,6 +19,7 @@
 //   objective_kernel      evaluate_objective's assignment-cost sum + loads.
 //   generate_costs_kernel synthetic euclidean cost matrix, in place in HBM.
 #include <cub/cub.cuh>
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint)
 
 #include "common.cuh"
 
@@ -83,6 +84,135 @@ __global__ void __launch_bounds__(256) row_argmin_kernel(const int32_t* __restri
     gmax = max(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
   }
   if (lane == 0) {
+    atomicMin(reinterpret_cast<long long*>(&minmax[0]), static_cast<long long>(gmin));
+    atomicMax(reinterpret_cast<long long*>(&minmax[1]), static_cast<long long>(gmax));
+  }
+}
+
+// ---- the arrival scan through TMA ----
+// Persistent CTAs (one per SM) stream groups of 8 rows through a
+// `stages`-deep ring of shared-memory tiles: one elected thread issues
+// cp.async.bulk.tensor (TMA, 256-column x 8-row boxes of a 2D tensor map
+// over the matrix) that complete_tx on the stage's full mbarrier; warp w
+// reduces row w of the group from shared memory (128-bit loads, lanes over
+// the columns, shuffle argmin with the smallest id on ties) and releases the
+// stage through its empty mbarrier; a ninth warp only produces. Same
+// outputs as row_argmin_kernel.
+constexpr int kTmaRows = 16;     // rows per group (= consumer warps per CTA)
+constexpr int kTmaBoxCols = 256; // columns per TMA box (the box-dim limit)
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* b, unsigned phase) {
+  asm volatile("{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra W%=;\n}" ::"r"(smem_addr(b)), "r"(phase) : "memory");
+}
+
+template <int NCB>
+__global__ void __launch_bounds__(32 * (kTmaRows + 1), 1) row_argmin_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                int64_t n, int32_t k, int stages,
+                                                                int32_t* __restrict__ best_center,
+                                                                int64_t* __restrict__ keys,
+                                                                int64_t* __restrict__ minmax,
+                                                                int64_t id0) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  constexpr int kStageInts = NCB * kTmaRows * kTmaBoxCols;
+  int32_t* buf = reinterpret_cast<int32_t*>(tsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + static_cast<size_t>(stages) * kStageInts * 4);
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ngroups = (n + kTmaRows - 1) / kTmaRows;
+  const int64_t mine = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaRows);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int s, int64_t it) {
+    const int64_t g = blockIdx.x + it * gridDim.x;
+    const unsigned fb = smem_addr(&full[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                 "r"(static_cast<unsigned>(kStageInts * 4)) : "memory");
+#pragma unroll
+    for (int b = 0; b < NCB; ++b) {
+      const unsigned dst = smem_addr(buf + static_cast<size_t>(s) * kStageInts + b * kTmaRows * kTmaBoxCols);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+          ::"r"(dst), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(b * kTmaBoxCols),
+          "r"(static_cast<int>(g * kTmaRows)), "r"(fb) : "memory");
+    }
+  };
+  if (warp == kTmaRows) {
+    // producer warp: keep every stage of the ring in flight
+    if (lane == 0) {
+      for (int64_t it = 0; it < mine; ++it) {
+        const int s = static_cast<int>(it % stages);
+        if (it >= stages) mbar_wait_parity(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
+        issue(s, it);
+      }
+    }
+    return;
+  }
+  int32_t gmin = INT32_MAX, gmax = INT32_MIN;
+  for (int64_t it = 0; it < mine; ++it) {
+    const int s = static_cast<int>(it % stages);
+    const unsigned ph = static_cast<unsigned>((it / stages) & 1);
+    mbar_wait_parity(&full[s], ph);
+    const int64_t row = (blockIdx.x + it * gridDim.x) * kTmaRows + warp;
+    if (row < n) {
+      const int32_t* st = buf + static_cast<size_t>(s) * kStageInts + warp * kTmaBoxCols;
+      // two independent argmin chains (even / odd 16 B pieces), merged below
+      int32_t bv = INT32_MAX, bi = INT32_MAX, bv2 = INT32_MAX, bi2 = INT32_MAX;
+      int4 xs[2 * NCB];
+#pragma unroll
+      for (int b = 0; b < NCB; ++b) {
+        const int4* bx = reinterpret_cast<const int4*>(st + b * kTmaRows * kTmaBoxCols);
+        xs[2 * b] = bx[lane];
+        xs[2 * b + 1] = bx[lane + 32];
+      }
+#pragma unroll
+      for (int q = 0; q < 2 * NCB; ++q) {
+        const int c = (q >> 1) * kTmaBoxCols + 4 * (lane + 32 * (q & 1));
+        const int32_t e[4] = {xs[q].x, xs[q].y, xs[q].z, xs[q].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (c + i < k) {
+            if (q & 1) argmin_step(e[i], c + i, bv2, bi2);
+            else argmin_step(e[i], c + i, bv, bi);
+            gmin = min(gmin, e[i]);
+            gmax = max(gmax, e[i]);
+          }
+        }
+      }
+      argmin_step(bv2, bi2, bv, bi);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int32_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmin_step(ov, oi, bv, bi);
+      }
+      if (lane == 0) {
+        best_center[row] = bi;
+        keys[row] = static_cast<int64_t>(bv) * (int64_t(1) << 32) + (id0 + row);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[s])) : "memory");
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+    gmax = max(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+  }
+  if (lane == 0 && gmin != INT32_MAX) {
     atomicMin(reinterpret_cast<long long*>(&minmax[0]), static_cast<long long>(gmin));
     atomicMax(reinterpret_cast<long long*>(&minmax[1]), static_cast<long long>(gmax));
   }

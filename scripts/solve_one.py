@@ -25,6 +25,8 @@ p.add_argument("--theta", default="8/10")
 p.add_argument("--reps", type=int, default=1)
 p.add_argument("--golden", default=None)
 p.add_argument("--scan", action="store_true", help="also time the build_index scan")
+p.add_argument("--road", action="store_true",
+               help="configs[3]-style road-network instance (RoadSpec, host-generated)")
 a = p.parse_args()
 if a.golden:
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "scale", a.golden + ".json")))
@@ -34,7 +36,14 @@ else:
     spec = SI.SynthSpec(a.n, a.k, seed=a.seed, theta_num=tn, theta_den=td)
 print("lib", S.LIB_PATH, "engine", os.environ.get("LBDD_B200_ENGINE", "cluster"), spec.name(),
       flush=True)
-dev = S.DeviceInstance.from_spec(spec)
+if a.road:
+    spec = SI.RoadSpec(a.n, a.k, seed=a.seed)
+    print("road", spec.name(), flush=True)
+    t0 = time.time()
+    dev = S.DeviceInstance.upload(SI.road_problem(spec))
+    print(f"generated + uploaded in {time.time() - t0:.1f} s", flush=True)
+else:
+    dev = S.DeviceInstance.from_spec(spec)
 for r in range(a.reps):
     t = time.time()
     try:

@@ -184,3 +184,145 @@ def instance_sha256(cost_matrix: np.ndarray, spec: SynthSpec) -> str:
 
 def assignment_sha256(assignment) -> str:
     return hashlib.sha256(np.ascontiguousarray(assignment, dtype=np.int32).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# configs[3]: road-network-like distances ("lbdd-road-v1")
+# ---------------------------------------------------------------------------
+#
+# A road graph of V vertices: uniform random points in the unit square
+# (numpy PCG64 seeded with `seed`), each joined to its 6 nearest neighbours,
+# edge length = euclidean x a winding factor in [1, 1.5); components joined
+# to the largest by their nearest pair. Centers sit on k distinct vertices;
+# demand d sits on vertex stream(seed, 13, d) % V with an access length
+# (stream(seed, 14, d) >> 11) * 2^-53 * 0.01. The float32 cost is the
+# shortest-path length (scipy Dijkstra from every center) plus the access
+# length; the solver's integer cost is max(1, rint(1000 * float32 cost)),
+# the integerisation of the reference's own road-graph generator
+# (instgen.hpp:87-90, scaled_cost) -- the reference's Cost is int64
+# (core.hpp:16), so float costs reach it only integerised.
+# Capacities: theta = 9/10, weights 1 + (h % 1000)^2 // 1000 (heavily skewed).
+
+@dataclass(frozen=True)
+class RoadSpec:
+    n: int
+    k: int
+    seed: int = 20250
+    vertices: int = 16384
+    theta_num: int = 9
+    theta_den: int = 10
+    pen_lo: int = 1
+    pen_hi: int = 200
+
+    def name(self) -> str:
+        return (f"lbdd-road-v1(n={self.n},k={self.k},seed={self.seed},V={self.vertices},"
+                f"theta={self.theta_num}/{self.theta_den},pen=[{self.pen_lo},{self.pen_hi}])")
+
+
+CONFIG3 = RoadSpec(2_000_000, 1000)
+_ROAD_CACHE = {}
+
+
+def road_distances(spec: RoadSpec) -> np.ndarray:
+    """(V, k) float32 shortest-path lengths from every center vertex."""
+    key = (spec.seed, spec.vertices, spec.k)
+    if key in _ROAD_CACHE:
+        return _ROAD_CACHE[key]
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components, dijkstra
+    from scipy.spatial import cKDTree
+    V = spec.vertices
+    rng = np.random.default_rng(spec.seed)
+    pts = rng.random((V, 2))
+    tree = cKDTree(pts)
+    dd, idx = tree.query(pts, k=7)
+    rows = np.repeat(np.arange(V), 6)
+    cols = idx[:, 1:].reshape(-1)
+    w = dd[:, 1:].reshape(-1) * (1.0 + 0.5 * rng.random(V * 6))
+    g = csr_matrix((w, (rows, cols)), shape=(V, V))
+    g = g.maximum(g.T).tolil()
+    ncomp, lab = connected_components(g, directed=False)
+    if ncomp > 1:
+        big = np.bincount(lab).argmax()
+        main = np.nonzero(lab == big)[0]
+        mtree = cKDTree(pts[main])
+        for c in range(ncomp):
+            if c == big:
+                continue
+            mem = np.nonzero(lab == c)[0]
+            dist, j = mtree.query(pts[mem])
+            i = int(np.argmin(dist))
+            a, b = int(mem[i]), int(main[j[i]])
+            g[a, b] = g[b, a] = float(dist[i]) * 1.25
+    g = g.tocsr()
+    centers = rng.choice(V, spec.k, replace=False)
+    D = dijkstra(g, indices=centers).T.astype(np.float32)
+    _ROAD_CACHE[key] = D
+    return D
+
+
+def road_float_rows(spec: RoadSpec, row0: int, rows: int) -> np.ndarray:
+    D = road_distances(spec)
+    v = (stream_np(spec.seed, 13, row0, rows) % np.uint64(spec.vertices)).astype(np.int64)
+    acc = ((stream_np(spec.seed, 14, row0, rows) >> np.uint64(11)).astype(np.float64)
+           * 2.0 ** -53 * 0.01).astype(np.float32)
+    return D[v] + acc[:, None]
+
+
+def road_cost_rows(spec: RoadSpec, row0: int, rows: int, out: np.ndarray | None = None):
+    c = np.rint(road_float_rows(spec, row0, rows).astype(np.float64) * 1000.0)
+    np.maximum(c, 1.0, out=c)
+    if out is None:
+        return c.astype(np.int32)
+    out[...] = c
+    return out
+
+
+def road_costs(spec: RoadSpec, out: np.ndarray | None = None, chunk: int = 16384,
+               threads: int | None = None) -> np.ndarray:
+    if out is None:
+        out = np.empty((spec.n, spec.k), np.int32)
+    road_distances(spec)  # build once, outside the threads
+    threads = threads or min(16, os.cpu_count() or 1)
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda r0: road_cost_rows(spec, r0, min(chunk, spec.n - r0),
+                                              out[r0:r0 + min(chunk, spec.n - r0)]),
+                    range(0, spec.n, chunk)))
+    return out
+
+
+def road_centers(spec: RoadSpec):
+    k = spec.k
+    total = spec.n * spec.theta_num // spec.theta_den
+    w = [1 + (stream_int(spec.seed, 15, s) % 1000) ** 2 // 1000 for s in range(k)]
+    W = sum(w)
+    cap = [total * ws // W for ws in w]
+    for s in range(total - sum(cap)):
+        cap[s] += 1
+    span = spec.pen_hi - spec.pen_lo + 1
+    fam, off, par = [], [0], []
+    for s in range(k):
+        p = stream_int(spec.seed, 16, s)
+        f = p % 3
+        base = spec.pen_lo + (p >> 8) % span
+        fam.append(f)
+        if f == 0:
+            par.append(base)
+        elif f == 1:
+            par += [base, (p >> 24) % 6]
+        else:
+            v = base
+            par.append(v)
+            for t in range(1, 4):
+                v += (p >> (32 + 3 * t)) % 8
+                par.append(v)
+        off.append(len(par))
+    return (np.array(cap, np.int64), np.array(fam, np.int32), np.array(off, np.int64),
+            np.array(par, np.int64))
+
+
+def road_problem(spec: RoadSpec):
+    from paper_2304_06543_b200.instance import ProblemInstance
+    cap, fam, off, par = road_centers(spec)
+    params = [list(par[off[i]:off[i + 1]]) for i in range(spec.k)]
+    return ProblemInstance.from_arrays(road_costs(spec), cap, fam, params)

@@ -249,3 +249,28 @@ def test_grid_engine_matches_oracle(dev, oracle, monkeypatch):
             opts = SolverOptions(refine_to_fixpoint=bool(it % 2))
             assert same_report(dev.solve(inst, solver, opts), oracle.solve(inst, solver, opts)), \
                 (it, solver, n, k, max_cost)
+
+
+def test_road_network_instances_match_reference(dev):
+    """configs[3]-shaped road-network instances (synth_instances RoadSpec:
+    shortest paths on a random road graph, float32 costs integerised like
+    instgen.hpp:87-90, heavily skewed capacities) against goldens of the
+    UNMODIFIED reference (tests/golden/make_road_golden.py): bit-exact
+    objective and assignment; the float32 objective under that assignment
+    then agrees too (here within 1e-6 relative, the north_star tolerance)."""
+    import synth_instances as SI
+    from paper_2304_06543_b200.instance import SolverOptions
+    from conftest import load_golden
+    for entry in load_golden("road_v1.json"):
+        spec = SI.RoadSpec(**entry["spec"])
+        prob = SI.road_problem(spec)
+        for tag, opts in [("asral", SolverOptions()),
+                          ("asral_fixpoint", SolverOptions(refine_to_fixpoint=True))]:
+            want = entry["reports"][tag]
+            got = dev.asral_solve(prob, opts)
+            assert got.objective == want["objective"], (spec.name(), tag)
+            assert SI.assignment_sha256(got.assignment) == want["assignment_sha256"]
+            f = SI.road_float_rows(spec, 0, spec.n).astype(np.float64)
+            ints = prob.costs.astype(np.int64)[np.arange(spec.n), got.assignment].sum()
+            fobj = 1000.0 * f[np.arange(spec.n), got.assignment].sum() + (got.objective - int(ints))
+            assert abs(fobj - want["float_objective"]) <= 1e-6 * abs(want["float_objective"])

@@ -151,6 +151,7 @@ struct lbdd_b200_instance {
   DevBuf<int32_t> dirty, log_d, log_to, log_n, add_ids, add_cnt;
   DevBuf<int64_t> MX;
   DevBuf<uint8_t> LN;
+  DevBuf<int16_t> ktile;  // global key tile (tile_mode 2)
   int cluster_size = 0;  // chosen once per instance
   // CUDA-event kernel times of the current solve (reported per solve)
   int64_t engine_ns = 0, engine_launches = 0, row_scan_ns = 0;
@@ -186,7 +187,7 @@ struct lbdd_b200_instance {
     single_out.release(); rowver.release(); load.release(); dummies.release(); M.release();
     pi.release(); dirty.release(); log_d.release(); log_to.release(); log_n.release();
     add_ids.release(); add_cnt.release();
-    MX.release(); LN.release();
+    MX.release(); LN.release(); ktile.release();
     colW.release();
     single_gain.release(); ctl.release(); bar.release(); path.release(); dumflag.release();
     ib_cnt.release(); ib_off.release(); ib_cursor.release(); ib_sorted.release();
@@ -835,8 +836,19 @@ EngineCtl run_cluster_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begi
   }
   const int cs = I->cluster_size;
   const int s = (k + 1 + cs - 1) / cs;
-  const bool tile = keys16 && cluster_smem_bytes(k, s, block, true) <= 220 * 1024;
-  A.tile_mode = tile ? 1 : 0;
+  const char* gf = std::getenv("LBDD_B200_GTILE_FORCE");  // tests: the global tile at any k
+  const bool force_g = gf != nullptr && std::string(gf) == "1";
+  const bool tile = keys16 && !force_g && cluster_smem_bytes(k, s, block, true) <= 220 * 1024;
+  // keys that fit int16 but a tile that does not fit shared memory: the
+  // same tile in global memory (k x k int16: 8 MB at k = 2000, L2-resident)
+  // instead of reading the int64 heads of M
+  const char* gt = std::getenv("LBDD_B200_GTILE");
+  const bool gtile = !tile && keys16 && !(gt != nullptr && std::string(gt) == "0");
+  A.tile_mode = tile ? 1 : (gtile ? 2 : 0);
+  if (gtile) {
+    I->ktile.ensure(static_cast<size_t>(k) * k);
+    A.ktile = I->ktile.p;
+  }
   const size_t smem = cluster_smem_bytes(k, s, block, tile);
   CUDA_OK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));

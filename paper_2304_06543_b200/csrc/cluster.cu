@@ -237,7 +237,9 @@ struct Ctx {
   unsigned rph;       // phase bits of the round mbarriers S.rmb[0], S.rmb[1]
   int err;            // sticky, identical in all CTAs (read at exchanges)
   bool lead;          // rank 0, thread 0
-  bool tile;          // keys of my columns resident in S.wt
+  bool tile;          // int16 transfer keys of my columns in a tile (X.wt)
+  int16_t* wt;        // tile of my columns: key of (u, v0 + col) at wt[u * wst + col];
+  int wst;            //   shared memory (stride s) or, when that does not fit, global (stride k)
   // per-launch counters kept in registers (lead thread), flushed at exit so
   // no global read-modify-write sits on a round's critical path
   int64_t n_barriers;
@@ -413,7 +415,7 @@ __device__ void validate_lists(Ctx& X, int where) {
                pe.kind, pe.demand, A.inv_cnt[i]);
       }
     }
-    if (X.tile && X.S.wt[static_cast<int64_t>(u) * X.s + (j - X.v0)] != key16(t.e[0]))
+    if (X.tile && X.wt[static_cast<int64_t>(u) * X.wst + (j - X.v0)] != key16(t.e[0]))
       set_err(X, 320 + where, u);
   }
   __syncthreads();
@@ -731,10 +733,10 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
     if (X.tile && X.A.dummies == nullptr) {
       // asral: no placeholder flags. cand < min(bound, best) is tested as
       // lp + w * unit < lim with lim = min(bound, best) - base, shrinking
-      const int16_t* wcol = S.wt + col;
+      const int16_t* wcol = X.wt + col;
       const int64_t lim0 = bound - base;
       int64_t lim = lim0;
-      const int sw = X.s;  // nd * s < 2^31: 32-bit index math
+      const int sw = X.wst;  // nd * wst < 2^31: 32-bit index math
       int t = ty;
       // four independent (entry, key) load pairs in flight per iteration
       for (; t + 3 * rpp < cnt; t += 4 * rpp) {
@@ -757,7 +759,7 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
       for (int t = ty; t < cnt; t += rpp) {
         const FEntry e = cmp[t];
         const int u = fe_node(e);
-        const int64_t w = key16_weight(S.wt[static_cast<int64_t>(u) * X.s + col], fe_dum(e));
+        const int64_t w = key16_weight(X.wt[static_cast<int64_t>(u) * X.wst + col], fe_dum(e));
         if (u == v || w == kNoEdge) continue;
         const int64_t cand = e.lp + w * kUnit + base;
         if (cand < bound && cand < best) best = cand;
@@ -999,7 +1001,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       const int r = list_remove(t, e.demand);
       if (r == 0) continue;
       list_store(A, idx, t);
-      if (X.tile && (r & 1)) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = key16(t.e[0]);
+      if (X.tile && (r & 1)) X.wt[static_cast<int64_t>(e.from_center) * X.wst + (j - X.v0)] = key16(t.e[0]);
       if (r & 2) {
         const int pos = atomicAdd(&A.inv_cnt[i], 1);
         A.inv_cols[static_cast<int64_t>(i) * k + pos] = j;
@@ -1016,7 +1018,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       const int64_t idx = static_cast<int64_t>(e.to_center) * k + j;
       TopK t = list_load(A, idx);
       if (list_insert(t, pack_transfer(row[j] - hv, e.demand))) {
-        if (X.tile) S.wt[static_cast<int64_t>(e.to_center) * X.s + (j - X.v0)] = key16(t.e[0]);
+        if (X.tile) X.wt[static_cast<int64_t>(e.to_center) * X.wst + (j - X.v0)] = key16(t.e[0]);
       }
       list_store(A, idx, t);
     }
@@ -1303,7 +1305,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       const int64_t* mx = A.MX + idx * 3;
       const int len = (m != kEmpty) + (mx[0] != kEmpty) + (mx[1] != kEmpty) + (mx[2] != kEmpty);
       A.LN[idx] = static_cast<uint8_t>(len | (len < kTopK ? 8 : 0));
-      if (X.tile) S.wt[static_cast<int64_t>(e.from_center) * X.s + (j - X.v0)] = key16(m);
+      if (X.tile) X.wt[static_cast<int64_t>(e.from_center) * X.wst + (j - X.v0)] = key16(m);
     }
   }
   __syncthreads();
@@ -1324,7 +1326,7 @@ __device__ __forceinline__ void certify(Ctx& X) {
     const bool dum = has_dummy(X, u);
     for (int v = X.v0 + threadIdx.x; v < min(X.v1, X.k); v += blockDim.x) {
       if (v == u) continue;
-      const int64_t w = X.tile ? key16_weight(X.S.wt[static_cast<int64_t>(u) * X.s + (v - X.v0)], dum)
+      const int64_t w = X.tile ? key16_weight(X.wt[static_cast<int64_t>(u) * X.wst + (v - X.v0)], dum)
                                : pair_weight(A.M[static_cast<int64_t>(u) * A.k + v], dum);
       if (w == kNoEdge) continue;
       if (w + piu - X.S.pis[v - X.v0] < 0) bad = true;
@@ -1388,7 +1390,14 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     X.tx = threadIdx.x % X.cpp;
     X.ty = threadIdx.x / X.cpp;
   }
-  X.S = carve(smem_raw, A.k, X.s, X.tile);
+  X.S = carve(smem_raw, A.k, X.s, A.tile_mode == 1);
+  if (A.tile_mode == 1) {
+    X.wt = X.S.wt;
+    X.wst = X.s;
+  } else {
+    X.wt = A.ktile != nullptr ? A.ktile + X.v0 : nullptr;
+    X.wst = A.k;
+  }
   X.par = 0;
   X.err = 0;
   X.lead = X.rank == 0 && threadIdx.x == 0;
@@ -1417,8 +1426,8 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       const int u = static_cast<int>(i / ns);
       const int col = static_cast<int>(i - static_cast<int64_t>(u) * ns);
       const int v = X.v0 + col;
-      S.wt[static_cast<int64_t>(u) * X.s + col] =
-          v < k ? key16(A.M[static_cast<int64_t>(u) * k + v]) : kNoKey16;
+      if (v < k) X.wt[static_cast<int64_t>(u) * X.wst + col] = key16(A.M[static_cast<int64_t>(u) * k + v]);
+      else if (A.tile_mode == 1) X.wt[static_cast<int64_t>(u) * X.wst + col] = kNoKey16;
     }
   }
   if (threadIdx.x < 16) S.misc[threadIdx.x] = 0;
@@ -1553,7 +1562,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         const int64_t idx = static_cast<int64_t>(s) * k + j;
         TopK t = list_load(A, idx);
         if (list_insert(t, pack_transfer(row[j] - hv, d))) {
-          if (X.tile) S.wt[static_cast<int64_t>(s) * X.s + (j - X.v0)] = key16(t.e[0]);
+          if (X.tile) X.wt[static_cast<int64_t>(s) * X.wst + (j - X.v0)] = key16(t.e[0]);
         }
         list_store(A, idx, t);
         const int64_t m = t.e[0];

@@ -197,7 +197,9 @@ struct EngineArgs {
   int32_t* rowslot;      // k, -1 when not a transfer source of the current path
   int32_t* src_list;     // k + 1 sources of the last applied path
   int32_t* rowver;       // k: bumped whenever row u of M changes
-  int32_t tile_mode;     // 1: each CTA caches its relaxation tile of M keys in smem
+  int32_t tile_mode;     // 1: each CTA caches its relaxation tile of M keys in smem;
+                         // 2: the same int16 tile, k x k, in global memory (L2)
+  int16_t* ktile;        // tile_mode 2: int16 key of M[u][v] at ktile[u * k + v]
   int32_t pad1;
   EngineCtl* ctl;
   GridBar* bar;

@@ -213,16 +213,17 @@ def test_reference_acceptance_suite_on_b200(criterion):
         out.stdout + out.stderr
 
 
-@pytest.mark.parametrize("tile", ["1", "0"])
+@pytest.mark.parametrize("tile", ["1", "0", "global"])
 def test_medium_solves_lists_rescans_and_key_paths(dev, oracle, tile, monkeypatch):
     """Mid-size random instances through the cluster engine: top-4 transfer
     lists, rescans over the bucket index + move log (LBDD_B200_CHUNK=64: many
     launches, so buckets are rebuilt and the log restarts often), the int16
     key tile (tile=1, narrow costs) and the global-key path (tile=0, or keys
     wider than int16). Bit-exact against the oracle."""
-    monkeypatch.setenv("LBDD_B200_TILE", tile)
+    monkeypatch.setenv("LBDD_B200_TILE", "1" if tile == "global" else tile)
+    monkeypatch.setenv("LBDD_B200_GTILE_FORCE", "1" if tile == "global" else "0")
     monkeypatch.setenv("LBDD_B200_CHUNK", "64")
-    rng = po.Mt19937_64(97 + int(tile))
+    rng = po.Mt19937_64(97 + {"1": 1, "0": 0, "global": 2}[tile])
     for it in range(6):
         n, k = 300 + rng() % 700, 20 + rng() % 140
         max_cost = [100, 5000, 200000][it % 3]

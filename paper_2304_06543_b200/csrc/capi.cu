@@ -633,7 +633,7 @@ void ensure_engine(lbdd_b200_instance* I, int64_t k_nodes) {
     for (int i = 0; i < 3; ++i) I->B[s][i].ensure(nodes);
   }
   I->colW.ensure(k + 1);
-  I->path.ensure(k + 1);
+  I->path.ensure(static_cast<size_t>(cl::kMaxCS) * (k + 1));  // one path copy per cluster CTA
   I->inv_cnt.ensure(k + 2);
   I->inv_cols.ensure((k + 1) * k);
   I->rowslot.ensure(k + 1);
@@ -760,12 +760,13 @@ EngineCtl run_engine(lbdd_b200_instance* I, EngineArgs A, int64_t a_begin, int64
 
 // ---- the cluster engine (cluster.cu): one thread-block cluster ----
 size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
-  return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * s + 2 * sizeof(cl::Pub) + 8 * 16 +
-         2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) + 8 * (k + 1) +
-         4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * static_cast<size_t>(cl::kMaxCS) * s + 4 * 3 * cl::kMaxSeg +
+  const size_t cin = static_cast<size_t>(cl::inbox_cap(s));
+  return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * cin + 2 * sizeof(cl::Pub) + 8 * 16 +
+         2 * sizeof(cl::Pub) * cl::kMaxCS + sizeof(cl::Agg) +
+         4 * (cl::kMaxCS + 2) + sizeof(cl::FEntry) * cl::kMaxCS * cin + 4 * 3 * cl::kMaxSeg +
          4 * 2 * cl::kMaxMine + 4 * (2 * cl::kMaxSeg + 2) +
          8 * 16 + 8 * 16 + 8 * 4 + 8 * 2 +
-         sizeof(PathEdge) * (k + 1) + 12 * block + 4 * 16 +
+         12 * block + 4 * 16 +
          4 * static_cast<size_t>(cl::kRowSlots) * ((k + 31) / 32) +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16;
 }

@@ -48,7 +48,12 @@ constexpr int kStage = 256;            // frontier entries staged per pass
 constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
 constexpr int kMaxSeg = 32;            // source rows rescanned per apply via the index
 constexpr int kRowSlots = 8;           // source rows of a row-mode rescan (column bitmaps)
-constexpr int kMaxMine = 1024;         // invalidated (segment, column) pairs a CTA owns per rescan
+constexpr int kMaxMine = 1024;
+// frontier entries one CTA pushes per exchange (inbox slots per source):
+// changed nodes past it stay pending for a later round -- the Δ-stepping
+// hold-back mechanism -- so shared memory no longer grows with k
+constexpr int kInCap = 128;
+__host__ __device__ inline int inbox_cap(int s) { return s < kInCap ? s : kInCap; }         // invalidated (segment, column) pairs a CTA owns per rescan
 
 // A frontier entry as pushed into every CTA's inbox: the node (bit 31: a
 // surplus placeholder sits there, strict-mode edge rule) and its label with
@@ -98,7 +103,7 @@ struct Pair2 {
 struct CS {           // shared-memory layout of one CTA
   int64_t* lab;       // [s]
   int64_t* pis;       // [s]
-  Pair2<FEntry> inbox;  // [kMaxCS * s] each: entries pushed by CTA r at r * s
+  Pair2<FEntry> inbox;  // [kMaxCS * cin] each: entries pushed by CTA r at r * cin
   Pair2<Pub> pub;      // [1] each
   PathEdge* path;     // [k + 1]
   uint8_t* chg;       // [s]
@@ -114,7 +119,7 @@ struct CS {           // shared-memory layout of one CTA
 
   int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
   int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
-  FEntry* cmp;        // [kMaxCS * s] the pushed entries, compacted by the exchange
+  FEntry* cmp;        // [kMaxCS * cin] the pushed entries, compacted by the exchange
   int32_t* seg;       // [3 * kMaxSeg] rescan segments (slot, prefix end, bucket count)
   int32_t* mine;      // [kMaxMine] my invalidated columns of a rescan ((g << 16) | j, then j by segment)
   int32_t* mine2;     // [kMaxMine] scratch of the counting sort
@@ -133,15 +138,16 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   CS S;
   S.lab = reinterpret_cast<int64_t*>(p); p += 8 * s;
   S.pis = reinterpret_cast<int64_t*>(p); p += 8 * s;
-  S.inbox = {reinterpret_cast<FEntry*>(p), kMaxCS * s}; p += 2 * sizeof(FEntry) * kMaxCS * s;
-  S.cmp = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * static_cast<size_t>(kMaxCS) * s;
+  const int cin = inbox_cap(s);
+  S.inbox = {reinterpret_cast<FEntry*>(p), kMaxCS * cin}; p += 2 * sizeof(FEntry) * kMaxCS * cin;
+  S.cmp = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * static_cast<size_t>(kMaxCS) * cin;
   S.pub = {reinterpret_cast<Pub*>(p), 1}; p += 2 * sizeof(Pub);
   S.red = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.allb = {reinterpret_cast<Pub*>(p), kMaxCS}; p += 2 * sizeof(Pub) * kMaxCS;
   S.all = S.allb[0];
   S.agg = reinterpret_cast<Agg*>(p); p += sizeof(Agg);
 
-  S.sinkw = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(k + 1);
+  S.sinkw = nullptr;  // global (EngineArgs::colW), set in the kernel prologue
   S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
   S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 3 * kMaxSeg;
   S.mine = reinterpret_cast<int32_t*>(p); p += 4 * kMaxMine;
@@ -152,7 +158,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.cw = reinterpret_cast<int64_t*>(p); p += 8 * 4;
   S.rmb = reinterpret_cast<uint64_t*>(p); p += 8 * 2;
-  S.path = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * (k + 1);
+  S.path = nullptr;   // global, one slice per CTA (EngineArgs::path), see the prologue
   S.qd = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
   S.qs = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
   S.qh = reinterpret_cast<int32_t*>(p); p += 4 * blockDim.x;
@@ -233,6 +239,7 @@ struct Ctx {
   CS S;
   cg::cluster_group cluster;
   int rank, csz, k, s, v0, v1;
+  int cin;            // inbox slots per source CTA (inbox_cap(s))
   int par;
   unsigned rph;       // phase bits of the round mbarriers S.rmb[0], S.rmb[1]
   int err;            // sticky, identical in all CTAs (read at exchanges)
@@ -551,7 +558,7 @@ __device__ __forceinline__ void exchange_finish(Ctx& X) {
     int c = 0, e = 0;
     if (lane < X.csz) {
       const Pub& p = S.all[lane];
-      c = (p.count >= 0 && p.count <= X.s) ? p.count : 0;
+      c = (p.count >= 0 && p.count <= X.cin) ? p.count : 0;
       e = p.err;
     }
     int incl = c;
@@ -598,7 +605,7 @@ __device__ __forceinline__ void exchange_finish(Ctx& X) {
       const int mid = (lo + hi) >> 1;
       if (S.pref[mid] <= g) lo = mid; else hi = mid;
     }
-    S.cmp[g] = S.inbox[X.par][lo * X.s + (g - S.pref[lo])];
+    S.cmp[g] = S.inbox[X.par][lo * X.cin + (g - S.pref[lo])];
   }
   X.err |= S.misc[4];
   __syncthreads();
@@ -627,7 +634,7 @@ __device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label
   e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
   e.pad = 0;
   e.lp = ((label & ~kParMask) | v) + pi * kLUnit;  // a candidate's parent field = v
-  const int slot = X.rank * X.s + pos;
+  const int slot = X.rank * X.cin + pos;
   for (int r = 0; r < X.csz; ++r) {
     FEntry* box = X.cluster.map_shared_rank(X.S.inbox[X.par], r);
     box[slot] = e;
@@ -640,7 +647,7 @@ __device__ __forceinline__ void push_entry_async(Ctx& X, int pos, int v, int64_t
   e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
   e.pad = 0;
   e.lp = ((label & ~kParMask) | v) + pi * kLUnit;
-  const unsigned src = smem_u32(&X.S.inbox[X.par][X.rank * X.s + pos]);
+  const unsigned src = smem_u32(&X.S.inbox[X.par][X.rank * X.cin + pos]);
   const unsigned bar = smem_u32(&X.S.rmb[X.par]);
   for (int r = 0; r < X.csz; ++r) st_async16(mapa_u32(src, r), &e, mapa_u32(bar, r));
 }
@@ -666,9 +673,14 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
       atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
       continue;
     }
+    const int pos = atomicAdd(&S.misc[1], 1);
+    if (pos >= X.cin) {  // inbox slots exhausted this round: held back (pending)
+      atomicAdd(&S.misc[3], 1);
+      atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
+      continue;
+    }
     S.chg[i] = 0;
     atomicMin(reinterpret_cast<long long*>(&S.red[3]), static_cast<long long>(label));
-    const int pos = atomicAdd(&S.misc[1], 1);
     if (async) push_entry_async(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
     else push_entry(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
     if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
@@ -676,7 +688,7 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
   __syncthreads();
   if (threadIdx.x == 0) {
     Pub* p = S.pub[X.par];
-    p->count = S.misc[1];
+    p->count = min(S.misc[1], X.cin);
     p->pending = S.misc[3];
     p->pmin = S.red[2];
     p->omin = min(S.red[2], S.red[3]);
@@ -879,7 +891,7 @@ __device__ __forceinline__ int64_t pi_of(Ctx& X, int v) {
 // Push the sources (label 0) owned by this CTA into every inbox[par].
 __device__ __forceinline__ void publish_sources(Ctx& X, const int* nodes, int count, int kind) {
   if (threadIdx.x == 0) {
-    int c = 0;
+    int c = 0, held = 0;
     for (int i = 0; i < count; ++i) {
       const int v = nodes[i];
       if (v < X.v0 || v >= X.v1) continue;
@@ -887,11 +899,17 @@ __device__ __forceinline__ void publish_sources(Ctx& X, const int* nodes, int co
       for (int j = 0; j < i; ++j) dup |= nodes[j] == v;
       if (dup) continue;
       X.S.lab[v - X.v0] = 0;
-      push_entry(X, c++, v, 0, X.S.pis[v - X.v0], kind != kPath && has_dummy(X, v));
+      if (c < X.cin) {
+        push_entry(X, c++, v, 0, X.S.pis[v - X.v0], kind != kPath && has_dummy(X, v));
+      } else {  // no inbox slot left: a pending source, pushed by a later round
+        X.S.chg[v - X.v0] = 1;
+        ++held;
+      }
     }
     X.S.pub[X.par]->count = c;
-    X.S.pub[X.par]->pending = 0;
-    X.S.pub[X.par]->omin = c > 0 ? 0 : kLabInf;
+    X.S.pub[X.par]->pending = held;
+    X.S.pub[X.par]->pmin = held ? 0 : kLabInf;
+    X.S.pub[X.par]->omin = (c > 0 || held > 0) ? 0 : kLabInf;
     X.S.pub[X.par]->sinklab = kLabInf;
   }
 }
@@ -1391,6 +1409,11 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     X.ty = threadIdx.x / X.cpp;
   }
   X.S = carve(smem_raw, A.k, X.s, A.tile_mode == 1);
+  X.cin = inbox_cap(X.s);
+  // O(k) per-search state outside shared memory (L1/L2): the weights into
+  // anchor-in (read only by their owner) and each CTA's copy of the path
+  X.S.sinkw = A.colW;
+  X.S.path = A.path + static_cast<int64_t>(X.rank) * (A.k + 1);
   if (A.tile_mode == 1) {
     X.wt = X.S.wt;
     X.wst = X.s;

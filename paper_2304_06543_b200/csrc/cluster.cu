@@ -254,6 +254,14 @@ struct Ctx {
   int64_t T;          // Δ-stepping threshold of the running search (packed)
   int64_t delta;      // Δ in packed units (of the running search)
   int64_t delta_main, delta_path;
+  // sink-bound pruning of the running search: a node whose distance d
+  // satisfies d + prune_c > d(sink) can improve neither the sink through
+  // its own edge (rc into anchor-in >= prune_c) nor any descendant (rc >= 0
+  // elsewhere), so it is dropped from the frontier. Off for repairs (their
+  // labels repair π and must be exact everywhere).
+  bool prune;
+  int64_t prune_c;    // cycle: 0; path: C (cost units)
+  int64_t cur_slab;   // sink label of the running search after the last exchange
   int64_t* dbg;       // [16] shared-memory counters (lead thread)
   int cpp, rpp, tx, ty;  // relax thread layout (fixed per CTA)
   __device__ Ctx(const EngineArgs& a, const cg::cluster_group& c) : A(a), cluster(c) {}
@@ -668,6 +676,10 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
     const int v = X.v0 + i;
     if (v == X.k) { S.chg[i] = 0; continue; }  // anchor-in has no out-edges
     const int64_t label = S.lab[i];
+    if (X.prune && X.cur_slab != kLabInf && lab_d(label) + X.prune_c > lab_d(X.cur_slab)) {
+      S.chg[i] = 0;  // cannot lead to a better sink label
+      continue;
+    }
     if (label > X.T) {
       atomicAdd(&S.misc[3], 1);
       atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
@@ -859,6 +871,7 @@ __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64
     collect(X, kind, anchor, true);
     PROF_MARK(X, 2);
     exchange_async(X);
+    X.cur_slab = X.S.agg->sinklab;
     advance_threshold(X);
     PROF_MARK(X, 3);
     ++rounds;
@@ -874,6 +887,7 @@ __device__ __forceinline__ int64_t sink_label(const Ctx& X) {
 // Start a search: labels of owned nodes to +inf, π(anchor-in) := π(anchor).
 __device__ __forceinline__ void reset_labels(Ctx& X, int64_t pi_anchor) {
   X.T = X.delta;  // labels start at the source's 0
+  X.cur_slab = kLabInf;
   for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
     X.S.lab[i] = kLabInf;
     X.S.chg[i] = 0;
@@ -1430,6 +1444,9 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   X.delta_path = A.delta_path <= 0 ? kLabInf / 4 : (A.delta_path << kLabShift);
   X.delta = X.delta_main;
   X.T = X.delta;
+  X.prune = false;
+  X.prune_c = 0;
+  X.cur_slab = kLabInf;
   X.dbg = X.S.dbg;
   if (threadIdx.x < 16) X.dbg[threadIdx.x] = 0;
   if (threadIdx.x < 16) X.S.prof[threadIdx.x] = 0;
@@ -1619,6 +1636,8 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       refund = 0;
       bound = 0;
       sink_inc = kHop;  // cycle graph: rc >= 0 into anchor-in
+      X.prune = true;
+      X.prune_c = 0;
       after = kStAfterCycle;
       t_search = gtimer();
       stage = kStSearch;
@@ -1698,6 +1717,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       refund = 0;
       bound = 0;
       sink_inc = kLabInf;
+      X.prune = false;
       stage = kStSearch;
       continue;
     }
@@ -1768,6 +1788,8 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       exchange(X);
       kind = kPath;
       bound = (-C) * kLUnit;
+      X.prune = true;
+      X.prune_c = C;
       sink_inc = kHop - bound;  // path graph: rc_pen >= C into anchor-in
       t_search = gtimer();
       stage = kStSearch;

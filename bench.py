@@ -230,8 +230,9 @@ def cpu_estimate(meta, first_box_s, first_n, steady_box_s_per_arrival):
     t_ck_here = meta["checkpoint"]["loop_s_here"]
     covered = len(marks) * every
     t_covered = marks[-1]
-    w = max(1, min(len(marks) - 1, 4))
-    tail_rate = (marks[-1] - marks[-1 - w]) / (w * every)
+    # the last window's rate: the per-arrival cost keeps growing, so this is
+    # the tightest lower bound the profile supports
+    tail_rate = (marks[-1] - marks[-2]) / every if len(marks) > 1 else marks[-1] / every
     t_full_here = t_covered + tail_rate * max(0, n - covered)
     # phase 1 (0 .. X) at the early speed ratio, the rest at the steady ratio
     est = (meta["setup_s_here"] * speed_first + t_ck_here * speed_first

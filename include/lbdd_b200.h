@@ -180,6 +180,20 @@ lbdd_status lbdd_b200_solve(lbdd_b200_instance* inst, int32_t solver,
                             lbdd_solve_report* report, int32_t* assignment_out,
                             int64_t* load_out);
 
+/* The first `arrivals` iterations of asral_solve's arrival loop
+ * (solver.hpp:143-166): the allotment the reference's SolverState holds
+ * after that many `index.insert` + refine steps (its checkpoints:
+ * oracle/ref_capi.cpp lbdd_ref_asral_run). assignment_out gets -1 for
+ * demands that have not arrived; report->objective is the partial
+ * objective (evaluate_partial_objective, core.hpp:216-233), checked
+ * against the engine's running delta. arrivals >= n is a full solve
+ * without the completeness check. Pins parity at scale against the
+ * reference's own mid-solve checkpoints. */
+lbdd_status lbdd_b200_solve_prefix(lbdd_b200_instance* inst,
+                                   const lbdd_solver_options* opts,
+                                   int64_t arrivals, lbdd_solve_report* report,
+                                   int32_t* assignment_out, int64_t* load_out);
+
 /* build_index (subspace.hpp:233) for a given allotment — the full
  * segmented-argmin scan of the cost matrix. Writes the k*k minimum-transfer
  * matrix: entry [from*k+to] = (cost << 32) | demand as int64 for the

@@ -963,7 +963,8 @@ void copy_out(lbdd_b200_instance* I, const int32_t* d_assign, int32_t* assignmen
 
 // asral_solve (solver.hpp:133-170)
 void solve_asral(lbdd_b200_instance* I, const lbdd_solver_options* o, int32_t solver,
-                 lbdd_solve_report* rep, int32_t* assignment_out, int64_t* load_out) {
+                 lbdd_solve_report* rep, int32_t* assignment_out, int64_t* load_out,
+                 int64_t arrivals = -1) {
   const int64_t start = now_ns();
   validate_centers(I);
   check_device_range(I);
@@ -976,9 +977,18 @@ void solve_asral(lbdd_b200_instance* I, const lbdd_solver_options* o, int32_t so
   A.best_center = I->best_center.p;
   A.fixpoint = o && o->refine_to_fixpoint;
   A.check_invariants = o && o->check_invariants;
-  const EngineCtl ctl = run_solver_engine(I, A, 0, I->n, keys_fit_int16(I));
+  const int64_t a_end = arrivals < 0 ? I->n : std::min<int64_t>(arrivals, I->n);
+  const EngineCtl ctl = run_solver_engine(I, A, 0, a_end, keys_fit_int16(I));
   std::vector<int64_t> loads;
-  rep->objective = finish(I, ctl.delta, loads);
+  if (a_end == I->n) {
+    rep->objective = finish(I, ctl.delta, loads);
+  } else {
+    // a prefix of the arrival loop: the partial allotment's objective
+    // (evaluate_partial_objective, core.hpp:216-233) must equal the running delta
+    int32_t missing = 0;
+    rep->objective = device_objective(I, I->home.p, loads, &missing);
+    if (rep->objective != ctl.delta) raise(LBDD_ERR_LOGIC, "lbdd: tracked objective diverged from recount");
+  }
   fill_report_stats(rep, ctl);
   rep->solver = solver;
   copy_out(I, I->home.p, assignment_out, loads, load_out);
@@ -1379,6 +1389,21 @@ lbdd_status lbdd_b200_solve(lbdd_b200_instance* inst, int32_t solver,
     report->row_scan_ns = inst->row_scan_ns;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+  });
+}
+
+lbdd_status lbdd_b200_solve_prefix(lbdd_b200_instance* inst, const lbdd_solver_options* opts,
+                                   int64_t arrivals, lbdd_solve_report* report,
+                                   int32_t* assignment_out, int64_t* load_out) {
+  return guarded([&] {
+    if (arrivals < 0) raise(LBDD_ERR_INVALID_ARGUMENT, "lbdd_b200: negative arrival count");
+    CUDA_OK(cudaSetDevice(inst->device));
+    std::memset(report, 0, sizeof(*report));
+    inst->engine_ns = inst->engine_launches = inst->row_scan_ns = 0;
+    solve_asral(inst, opts, LBDD_SOLVER_ASRAL, report, assignment_out, load_out, arrivals);
+    report->engine_ns = inst->engine_ns;
+    report->engine_launches = inst->engine_launches;
+    report->row_scan_ns = inst->row_scan_ns;
   });
 }
 

@@ -48,6 +48,8 @@ _lib.lbdd_b200_instance_centers.argtypes = [_P, _abi.I64P, _abi.I32P, _abi.I64P,
 _lib.lbdd_b200_instance_costs.argtypes = [_P, C.c_int64, C.c_int64, _abi.I32P]
 _lib.lbdd_b200_solve.argtypes = [_P, C.c_int32, C.POINTER(_abi.SolverOptionsC),
                                  C.POINTER(_abi.SolveReportC), _abi.I32P, _abi.I64P]
+_lib.lbdd_b200_solve_prefix.argtypes = [_P, C.POINTER(_abi.SolverOptionsC), C.c_int64,
+                                        C.POINTER(_abi.SolveReportC), _abi.I32P, _abi.I64P]
 _lib.lbdd_b200_build_index.argtypes = [_P, _abi.I32P, C.c_int64, C.c_int64, _abi.I64P]
 _lib.lbdd_b200_build_index_device.argtypes = [_P, _P, C.c_int64, C.c_int64, _P, _P]
 _lib.lbdd_b200_build_index_shard.argtypes = [_P, _P, C.c_int64, _P, _P]
@@ -244,6 +246,28 @@ def asral_solve(inst: InstanceLike, opts: Optional[SolverOptions] = None,
     """asral_solve, solver.hpp:133 (para-asral when opts.parallel)."""
     sid = _abi.SOLVER_PARA_ASRAL if (opts is not None and opts.parallel) else _abi.SOLVER_ASRAL
     return _solve(inst, sid, opts, device, want_assignment)
+
+
+def asral_prefix(inst: InstanceLike, arrivals: int, opts: Optional[SolverOptions] = None,
+                 device: int = 0) -> SolveReport:
+    """The first `arrivals` iterations of asral_solve's arrival loop
+    (solver.hpp:143-166): the partial allotment (-1 = not arrived yet) the
+    reference's SolverState holds at that point, e.g. at one of its
+    checkpoints (oracle/ref_capi.cpp lbdd_ref_asral_run)."""
+    dev, owned = _as_device(inst, device)
+    try:
+        opts = opts or SolverOptions()
+        oc, keep = opts.to_c()
+        rep = _abi.SolveReportC()
+        assign = np.empty(dev.n, np.int32)
+        load = np.zeros(dev.k + 1, np.int64)
+        _check(_lib.lbdd_b200_solve_prefix(dev.handle, C.byref(oc), int(arrivals), C.byref(rep),
+                                           _i32(assign), _i64(load)))
+        del keep
+        return SolveReport.from_c(rep, assign, load[:dev.k])
+    finally:
+        if owned:
+            dev.close()
 
 
 def strict_solve(inst: InstanceLike, opts: Optional[SolverOptions] = None,

@@ -82,13 +82,6 @@ struct Pub {          // per-CTA published scalars of one exchange
 static_assert(sizeof(Pub) == 48, "Pub travels as three 16 B st.async");
 static_assert(sizeof(FEntry) == 16, "FEntry travels as one 16 B st.async");
 
-struct Agg {          // cluster-wide reductions of the last exchange (warp 0)
-  int32_t pending;    // sum of Pub::pending
-  int32_t pad;
-  int64_t pmin;       // min Pub::pmin
-  int64_t omin;       // min Pub::omin
-  int64_t sinklab;    // min Pub::sinklab
-};
 
 // A pair of equal-sized buffers selected by parity: base + i * stride, so
 // that CS has no dynamically indexed member array (which would force the
@@ -115,11 +108,14 @@ struct CS {           // shared-memory layout of one CTA
   int64_t* red;       // [16] reduction scratch
   Pub* all;           // every CTA's pub of the last exchange (= allb[par])
   Pair2<Pub> allb;     // [kMaxCS] each: pubs PUSHED by every CTA, by parity
-  Agg* agg;           // [1] reductions over all[] (computed once per exchange)
 
-  int64_t* sinkw;     // [k] weights into anchor-in (sink owner, per search)
-  int32_t* pref;      // [kMaxCS + 1] prefix of S.all[].count
-  FEntry* cmp;        // [kMaxCS * cin] the pushed entries, compacted by the exchange
+  int64_t* sinkc;     // [s] per owned node u: π(u) + w(u, anchor-in) - π(anchor-in) of
+                      //   the running search (kLabInf: no edge); the OWNER of u
+                      //   evaluates u's edge into anchor-in when it pushes u
+  int64_t* part;      // [max(blockDim, s)] relax partials: row ty of column col at ty * ns + col
+  int64_t* wred;      // [4 * 32] per-warp reductions of collect (pmin, omin, sink, -)
+  uint32_t* rin;      // [2 * kMaxCS] inbox[par] of CTA r in the cluster window (mapa, once)
+  uint32_t* rbar;     // [2 * kMaxCS] rmb[par] of CTA r in the cluster window
   int32_t* seg;       // [3 * kMaxSeg] rescan segments (slot, prefix end, bucket count)
   int32_t* mine;      // [kMaxMine] my invalidated columns of a rescan ((g << 16) | j, then j by segment)
   int32_t* mine2;     // [kMaxMine] scratch of the counting sort
@@ -140,15 +136,16 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.pis = reinterpret_cast<int64_t*>(p); p += 8 * s;
   const int cin = inbox_cap(s);
   S.inbox = {reinterpret_cast<FEntry*>(p), kMaxCS * cin}; p += 2 * sizeof(FEntry) * kMaxCS * cin;
-  S.cmp = reinterpret_cast<FEntry*>(p); p += sizeof(FEntry) * static_cast<size_t>(kMaxCS) * cin;
   S.pub = {reinterpret_cast<Pub*>(p), 1}; p += 2 * sizeof(Pub);
   S.red = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.allb = {reinterpret_cast<Pub*>(p), kMaxCS}; p += 2 * sizeof(Pub) * kMaxCS;
   S.all = S.allb[0];
-  S.agg = reinterpret_cast<Agg*>(p); p += sizeof(Agg);
 
-  S.sinkw = nullptr;  // global (EngineArgs::colW), set in the kernel prologue
-  S.pref = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxCS + 2);
+  S.sinkc = reinterpret_cast<int64_t*>(p); p += 8 * s;
+  S.part = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(max(static_cast<int>(blockDim.x), s));
+  S.wred = reinterpret_cast<int64_t*>(p); p += 8 * 4 * 32;
+  S.rin = reinterpret_cast<uint32_t*>(p); p += 4 * 2 * kMaxCS;
+  S.rbar = reinterpret_cast<uint32_t*>(p); p += 4 * 2 * kMaxCS;
   S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 3 * kMaxSeg;
   S.mine = reinterpret_cast<int32_t*>(p); p += 4 * kMaxMine;
   S.mine2 = reinterpret_cast<int32_t*>(p); p += 4 * kMaxMine;
@@ -264,6 +261,14 @@ struct Ctx {
   int64_t cur_slab;   // sink label of the running search after the last exchange
   int64_t* dbg;       // [16] shared-memory counters (lead thread)
   int cpp, rpp, tx, ty;  // relax thread layout (fixed per CTA)
+  int cpar;           // parity of collect's slot counter (S.misc[8 + cpar])
+  // the last exchange, reduced by EVERY warp for itself (no CTA barrier, no
+  // shared copy): lane r < csz holds the inclusive prefix of the entry
+  // counts of CTAs 0..r (lanes >= csz: the total), so relax maps a flat
+  // entry index to (source CTA, slot) with one ballot
+  int xincl;
+  int xtotal, xpend;
+  int64_t xpmin, xomin, xslab;
   __device__ Ctx(const EngineArgs& a, const cg::cluster_group& c) : A(a), cluster(c) {}
 };
 
@@ -539,7 +544,9 @@ __device__ __forceinline__ void exchange_async(Ctx& X) {
       for (int q = 0; q < 3; ++q) {
         st_async16(dst + 16 * q, reinterpret_cast<const char*>(mine) + 16 * q, rbar);
       }
-      remote_arrive_tx(rbar, static_cast<unsigned>(sizeof(Pub) + sizeof(FEntry) * mine->count));
+      // collect wrote this CTA's own copy of its entries with plain stores
+      remote_arrive_tx(rbar, static_cast<unsigned>(sizeof(Pub) +
+                                                   (r == X.rank ? 0 : sizeof(FEntry) * mine->count)));
     }
   }
   long long tw0 = 0;
@@ -560,78 +567,65 @@ __device__ __forceinline__ void exchange_async(Ctx& X) {
 __device__ __forceinline__ void exchange_finish(Ctx& X) {
   CS& S = X.S;
   S.all = S.allb[X.par];
-  if (threadIdx.x < 32) {
-    // warp 0: scan the counts, OR the errors
-    const int lane = threadIdx.x;
-    int c = 0, e = 0;
-    if (lane < X.csz) {
-      const Pub& p = S.all[lane];
-      c = (p.count >= 0 && p.count <= X.cin) ? p.count : 0;
-      e = p.err;
-    }
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane < X.csz) S.pref[lane + 1] = incl;
-    if (lane == 0) S.pref[0] = 0;
-    const unsigned anyerr = __ballot_sync(0xffffffffu, e != 0);
-    if (lane == 0) S.misc[4] = anyerr != 0;
-    // the reductions every thread used to recompute from all[] each round
-    int pend = 0;
-    long long pmin = kLabInf, omin = kLabInf, slab = kLabInf;
-    if (lane < X.csz) {
-      const Pub& p = S.all[lane];
-      pend = p.pending;
-      pmin = p.pmin;
-      omin = p.omin;
-      slab = p.sinklab;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      pend += __shfl_xor_sync(0xffffffffu, pend, o);
-      pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
-      omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
-      slab = min(slab, __shfl_xor_sync(0xffffffffu, slab, o));
-    }
-    if (lane == 0) {
-      S.agg->pending = pend;
-      S.agg->pmin = pmin;
-      S.agg->omin = omin;
-      S.agg->sinklab = slab;
-    }
+  // every warp reduces the CTAs' pubs itself (identical results everywhere)
+  const int lane = threadIdx.x & 31;
+  int c = 0, e = 0, pend = 0;
+  long long pmin = kLabInf, omin = kLabInf, slab = kLabInf;
+  if (lane < X.csz) {
+    const Pub& p = S.all[lane];
+    c = (p.count >= 0 && p.count <= X.cin) ? p.count : 0;
+    e = p.err;
+    pend = p.pending;
+    pmin = p.pmin;
+    omin = p.omin;
+    slab = p.sinklab;
   }
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  X.xincl = incl;
+  X.xtotal = __shfl_sync(0xffffffffu, incl, 31);
+  if (__any_sync(0xffffffffu, e != 0)) X.err = 1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pend += __shfl_xor_sync(0xffffffffu, pend, o);
+    pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+    omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
+    slab = min(slab, __shfl_xor_sync(0xffffffffu, slab, o));
+  }
+  X.xpend = pend;
+  X.xpmin = pmin;
+  X.xomin = omin;
+  X.xslab = slab;
   if (X.lead) X.n_barriers += 1;
-  __syncthreads();
-  // flat index of the pushed entries: slot of the g-th entry in the inbox
-  const int total = S.pref[X.csz];
-  for (int g = threadIdx.x; g < total; g += blockDim.x) {
-    int lo = 0, hi = X.csz;  // last r with pref[r] <= g
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (S.pref[mid] <= g) lo = mid; else hi = mid;
-    }
-    S.cmp[g] = S.inbox[X.par][lo * X.cin + (g - S.pref[lo])];
-  }
-  X.err |= S.misc[4];
-  __syncthreads();
   // the next phase writes the other buffer while slow CTAs may still read
   // this one; it is rewritten only after the next barrier
   X.par ^= 1;
 }
 
-__device__ __forceinline__ int total_pending(const Ctx& X) { return X.S.agg->pending; }
+// Flat index t (warp-uniform) of the entries of the last exchange ->
+// inbox slot: segment = CTAs whose inclusive prefix is <= t.
+__device__ __forceinline__ int entry_slot(const Ctx& X, int t) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = __ballot_sync(0xffffffffu, lane < X.csz && X.xincl <= t);
+  const int seg = __popc(below);
+  const int excl = __shfl_sync(0xffffffffu, X.xincl, (seg + 31) & 31);
+  return seg * X.cin + t - (seg == 0 ? 0 : excl);
+}
+
+__device__ __forceinline__ int total_pending(const Ctx& X) { return X.xpend; }
 // next threshold: at least Δ above the smallest held-back label
 __device__ __forceinline__ void advance_threshold(Ctx& X) {
   if (total_pending(X) == 0) return;
-  const int64_t m = X.S.agg->pmin;
+  const int64_t m = X.xpmin;
   const int64_t t = m > kLabInf - X.delta ? kLabInf : m + X.delta;
   if (t > X.T) X.T = t;
 }
 
-__device__ __forceinline__ int total_count(const Ctx& X) { return X.S.pref[X.csz]; }
+__device__ __forceinline__ int total_count(const Ctx& X) { return X.xtotal; }
 
 // Push this CTA's changed nodes (and clear the flags) into every CTA's
 // inbox[par] (slot range rank * s): DSMEM stores, ordered before the
@@ -649,70 +643,158 @@ __device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label
   }
 }
 
-__device__ __forceinline__ void push_entry_async(Ctx& X, int pos, int v, int64_t label, int64_t pi,
-                                                 bool dum) {
-  FEntry e;
-  e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
-  e.pad = 0;
-  e.lp = ((label & ~kParMask) | v) + pi * kLUnit;
-  const unsigned src = smem_u32(&X.S.inbox[X.par][X.rank * X.cin + pos]);
-  const unsigned bar = smem_u32(&X.S.rmb[X.par]);
-  for (int r = 0; r < X.csz; ++r) st_async16(mapa_u32(src, r), &e, mapa_u32(bar, r));
-}
-
 // Δ-stepping: only improved nodes with label <= X.T are pushed; the rest
 // stay pending (their flag kept) and report their count and minimum.
-__device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async = false) {
+// merge: fold the relax partials of this round into the labels first (the
+// owner is the single writer of its labels: no shared-memory atomics).
+// Each pushed node's edge into anchor-in is evaluated here by its owner
+// (S.sinkc), so no CTA relaxes an anchor-in column; the CTA minimum of those
+// candidates is published as Pub::sinklab (running over the search).
+// async: the entries go out with st.async (the round exchange), one
+// (entry, destination) pair per thread; else with generic DSMEM stores.
+__device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async = false,
+                                        bool merge = false) {
   CS& S = X.S;
-  if (threadIdx.x == 0) {
-    S.misc[1] = 0;
-    S.misc[3] = 0;
-    S.red[2] = kLabInf;
-    S.red[3] = kLabInf;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
-    if (!S.chg[i]) continue;
+  // slots taken: S.misc[8 + cpar], zero here (reset by the previous call,
+  // whose own counter every thread read before the CTA barrier that
+  // separates the two calls); the other parity is reset for the next call
+  int* slots = &S.misc[8 + X.cpar];
+  if (threadIdx.x == 0) S.misc[8 + (X.cpar ^ 1)] = 0;
+  X.cpar ^= 1;
+  const int ns = X.v1 - X.v0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warps holding owned nodes (all of them when ns > blockDim)
+  const int nwa = min(static_cast<int>(blockDim.x + 31) >> 5, (ns + 31) >> 5);
+  long long pmin = kLabInf, omin = kLabInf, smin = kLabInf;
+  int held = 0;
+  if (warp < nwa)
+  for (int i0 = 0; i0 < ns; i0 += blockDim.x) {  // warp-uniform trip count
+    const int i = i0 + threadIdx.x;
+    bool push = false;
+    int64_t label = kLabInf;
     const int v = X.v0 + i;
-    if (v == X.k) { S.chg[i] = 0; continue; }  // anchor-in has no out-edges
-    const int64_t label = S.lab[i];
-    if (X.prune && X.cur_slab != kLabInf && lab_d(label) + X.prune_c > lab_d(X.cur_slab)) {
-      S.chg[i] = 0;  // cannot lead to a better sink label
-      continue;
+    if (i < ns) {
+      label = S.lab[i];
+      bool chg = S.chg[i] != 0;
+      if (merge && v < X.k) {
+        int64_t best = kLabInf;
+        for (int r = 0; r < X.rpp; ++r) best = min(best, S.part[r * ns + i]);
+        if (best < label) {
+          if ((best & ~kParMask) < (label & ~kParMask)) chg = true;
+          label = best;
+          S.lab[i] = best;
+        }
+      }
+      if (chg) {
+        if (v == X.k) {
+          chg = false;  // anchor-in has no out-edges
+        } else if (X.prune && X.cur_slab != kLabInf && lab_d(label) + X.prune_c > lab_d(X.cur_slab)) {
+          chg = false;  // cannot lead to a better sink label
+        } else if (label > X.T) {
+          ++held;
+          pmin = min(pmin, static_cast<long long>(label));
+        } else {
+          push = true;
+        }
+      }
+      S.chg[i] = chg;
     }
-    if (label > X.T) {
-      atomicAdd(&S.misc[3], 1);
-      atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
-      continue;
+    const unsigned bal = __ballot_sync(0xffffffffu, push);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(slots, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (push) {
+      const int pos = base + __popc(bal & ((1u << lane) - 1));
+      if (pos >= X.cin) {  // inbox slots exhausted this round: held back (pending)
+        ++held;
+        pmin = min(pmin, static_cast<long long>(label));
+      } else {
+        S.chg[i] = 0;
+        omin = min(omin, static_cast<long long>(label));
+        const bool dum = kind != kPath && has_dummy(X, v);
+        FEntry e;
+        e.nd = v | (dum ? static_cast<int32_t>(0x80000000u) : 0);
+        e.pad = 0;
+        e.lp = ((label & ~kParMask) | v) + S.pis[i] * kLUnit;
+        if (async) S.inbox[X.par][X.rank * X.cin + pos] = e;
+        else push_entry(X, pos, v, label, S.pis[i], dum);
+        if (kind != kRepair) {
+          const int64_t sc = S.sinkc[i];
+          if (sc != kLabInf) {
+            const int64_t cand = ((label & ~kParMask) | v) + sc * kLUnit + kHop;
+            if (cand < 0) smin = min(smin, static_cast<long long>(cand));  // bound_sink = 0
+          }
+        }
+        if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
+      }
     }
-    const int pos = atomicAdd(&S.misc[1], 1);
-    if (pos >= X.cin) {  // inbox slots exhausted this round: held back (pending)
-      atomicAdd(&S.misc[3], 1);
-      atomicMin(reinterpret_cast<long long*>(&S.red[2]), static_cast<long long>(label));
-      continue;
+  }
+  if (warp < nwa) {
+    // most rounds change few nodes: reduce only what is there
+    if (__any_sync(0xffffffffu, held != 0)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+        held += __shfl_xor_sync(0xffffffffu, held, o);
+      }
     }
-    S.chg[i] = 0;
-    atomicMin(reinterpret_cast<long long*>(&S.red[3]), static_cast<long long>(label));
-    if (async) push_entry_async(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
-    else push_entry(X, pos, v, label, S.pis[i], kind != kPath && has_dummy(X, v));
-    if (lab_h(label) > X.k + 1) set_err(X, kErrNegCycleWitness, v);
+    if (__any_sync(0xffffffffu, omin != kLabInf)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
+    }
+    if (__any_sync(0xffffffffu, smin != kLabInf)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+    }
+    if (lane == 0) {
+      S.wred[warp] = pmin;
+      S.wred[32 + warp] = omin;
+      S.wred[64 + warp] = smin;
+      S.wred[96 + warp] = held;
+    }
   }
   __syncthreads();
+  const int cnt = min(*slots, X.cin);
+  if (async && cnt > 0) {
+    // (entry, destination) pairs over the CTA; this CTA's own copy is local
+    const int nd = X.csz - 1;
+    const unsigned off0 = static_cast<unsigned>(sizeof(FEntry)) * (X.rank * X.cin);
+    for (int q = threadIdx.x; q < cnt * nd; q += blockDim.x) {
+      const int e = q / nd, rr = q - e * nd;
+      const int r = rr < X.rank ? rr : rr + 1;
+      const unsigned off = off0 + static_cast<unsigned>(sizeof(FEntry)) * e;
+      const int4 v = *reinterpret_cast<const int4*>(&S.inbox[X.par][X.rank * X.cin + e]);
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                   ::"r"(S.rin[X.par * kMaxCS + r] + off), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w),
+                   "r"(S.rbar[X.par * kMaxCS + r]) : "memory");
+    }
+  }
   if (threadIdx.x == 0) {
+    long long pm = kLabInf, om = kLabInf, sm = kLabInf;
+    int hd = 0;
+    for (int w = 0; w < nwa; ++w) {
+      pm = min(pm, static_cast<long long>(S.wred[w]));
+      om = min(om, static_cast<long long>(S.wred[32 + w]));
+      sm = min(sm, static_cast<long long>(S.wred[64 + w]));
+      hd += static_cast<int>(S.wred[96 + w]);
+    }
     Pub* p = S.pub[X.par];
-    p->count = min(S.misc[1], X.cin);
-    p->pending = S.misc[3];
-    p->pmin = S.red[2];
-    p->omin = min(S.red[2], S.red[3]);
-    p->sinklab = (X.k >= X.v0 && X.k < X.v1) ? S.lab[X.k - X.v0] : kLabInf;
+    p->count = cnt;
+    p->pending = hd;
+    p->pmin = pm;
+    p->omin = min(pm, om);
+    if (sm < S.red[4]) S.red[4] = sm;
+    p->sinklab = S.red[4];
   }
 }
 
 // Relax every edge from the sources pushed in the last exchange into this
-// CTA's nodes. bound_mid / bound_sink: strict upper bounds on labels. Each
-// thread owns one destination column per pass and keeps its running
-// minimum in a register, so a column sees one shared-memory atomicMin per
-// pass; sources are read from the local inbox (broadcast within a warp).
+// CTA's nodes. bound_mid: strict upper bound on labels. Each thread owns
+// one destination column per pass and keeps its running minimum in a
+// register; the row partials go to S.part and collect folds them into the
+// labels (no 64-bit shared-memory atomics, which are CAS loops). Sources are
+// read from the local inbox (broadcast within a warp). Edges into anchor-in
+// are evaluated by the owners of their sources in collect.
 __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refund_a,
                                       int64_t bound_mid, int64_t bound_sink) {
   CS& S = X.S;
@@ -721,50 +803,32 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
   if (ns <= 0) return;  // uniform within the CTA
   const int cpp = X.cpp, rpp = X.rpp, tx = X.tx, ty = X.ty;
   constexpr int64_t kUnit = kLUnit;
-  const int cnt_all = S.pref[X.csz];
-  if (kind != kRepair && X.k >= X.v0 && X.k < X.v1) {
-    // anchor-in (sink) column: its weights come from S.sinkw, not the tile.
-    // Evaluated by the whole CTA in a separate pass, so no warp of the
-    // column loop below diverges into a second, scalar branch.
-    const int col = X.k - X.v0;
-    const int64_t base = kHop - S.pis[col] * kUnit;
-    int64_t best = kLabInf;
-    for (int t = threadIdx.x; t < cnt_all; t += blockDim.x) {
-      const FEntry e = S.cmp[t];
-      const int64_t w = S.sinkw[fe_node(e)];  // kNoEdge for the anchor itself
-      if (w == kNoEdge) continue;
-      const int64_t cand = e.lp + w * kUnit + base;
-      if (cand < bound_sink && cand < best) best = cand;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if ((threadIdx.x & 31) == 0 && best != kLabInf) {
-      const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
-                                      static_cast<long long>(best));
-      if ((best & ~kParMask) < (old & ~kParMask)) S.chg[col] = 1;
-    }
-  }
+  if (ty >= rpp) return;  // threads past the last full row of columns (whole warps)
+  // the entries of the last exchange, read in place (no compaction): flat
+  // index t -> slot by entry_slot (warp-uniform t: every lane of a warp has
+  // the same ty, cpp being a multiple of 32)
+  const FEntry* box = S.inbox[X.par ^ 1];
+  const int cnt = X.xtotal;
   for (int c0 = 0; c0 < ns; c0 += cpp) {
     const int col = c0 + tx;
     const int v = X.v0 + col;
-    if (col >= ns) continue;
-    if (v >= X.k || (kind != kRepair && v == anchor)) continue;
-    const int64_t base = kHop - S.pis[col] * kUnit;  // candidate = lp + w*unit + base
+    const bool valid = col < ns && v < X.k && !(kind != kRepair && v == anchor);
+    const int64_t base = valid ? kHop - S.pis[col] * kUnit : 0;  // candidate = lp + w*unit + base
     const int64_t bound = bound_mid;
     int64_t best = kLabInf;
-    const int cnt = S.pref[X.csz];
-    const FEntry* cmp = S.cmp;
     if (X.tile && X.A.dummies == nullptr) {
       // asral: no placeholder flags. cand < min(bound, best) is tested as
       // lp + w * unit < lim with lim = min(bound, best) - base, shrinking
-      const int16_t* wcol = X.wt + col;
+      const int16_t* wcol = X.wt + (valid ? col : 0);
       const int64_t lim0 = bound - base;
       int64_t lim = lim0;
       const int sw = X.wst;  // nd * wst < 2^31: 32-bit index math
       int t = ty;
       // four independent (entry, key) load pairs in flight per iteration
       for (; t + 3 * rpp < cnt; t += 4 * rpp) {
-        const FEntry e0 = cmp[t], e1 = cmp[t + rpp], e2 = cmp[t + 2 * rpp], e3 = cmp[t + 3 * rpp];
+        const int s0 = entry_slot(X, t), s1 = entry_slot(X, t + rpp);
+        const int s2 = entry_slot(X, t + 2 * rpp), s3 = entry_slot(X, t + 3 * rpp);
+        const FEntry e0 = box[s0], e1 = box[s1], e2 = box[s2], e3 = box[s3];
         const int16_t k0 = wcol[e0.nd * sw], k1 = wcol[e1.nd * sw];
         const int16_t k2 = wcol[e2.nd * sw], k3 = wcol[e3.nd * sw];
         if (k0 != kNoKey16 && e0.nd != v) lim = min(lim, e0.lp + static_cast<int64_t>(k0) * kUnit);
@@ -773,7 +837,7 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
         if (k3 != kNoKey16 && e3.nd != v) lim = min(lim, e3.lp + static_cast<int64_t>(k3) * kUnit);
       }
       for (; t < cnt; t += rpp) {
-        const FEntry e = cmp[t];
+        const FEntry e = box[entry_slot(X, t)];
         const int16_t key = wcol[e.nd * sw];
         if (key != kNoKey16 && e.nd != v) lim = min(lim, e.lp + static_cast<int64_t>(key) * kUnit);
       }
@@ -781,9 +845,10 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
     } else if (X.tile) {
 #pragma unroll 4
       for (int t = ty; t < cnt; t += rpp) {
-        const FEntry e = cmp[t];
+        const FEntry e = box[entry_slot(X, t)];
         const int u = fe_node(e);
-        const int64_t w = key16_weight(X.wt[static_cast<int64_t>(u) * X.wst + col], fe_dum(e));
+        const int64_t w = valid ? key16_weight(X.wt[static_cast<int64_t>(u) * X.wst + col], fe_dum(e))
+                                : kNoEdge;
         if (u == v || w == kNoEdge) continue;
         const int64_t cand = e.lp + w * kUnit + base;
         if (cand < bound && cand < best) best = cand;
@@ -798,9 +863,9 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
           const int tq = t + q * rpp;
           e[q].nd = -1;
           m[q] = kEmpty;
-          if (tq < cnt) {
-            e[q] = cmp[tq];
-            m[q] = A.M[static_cast<int64_t>(fe_node(e[q])) * A.k + v];
+          if (tq < cnt) {  // warp-uniform
+            e[q] = box[entry_slot(X, tq)];
+            if (valid) m[q] = A.M[static_cast<int64_t>(fe_node(e[q])) * A.k + v];
           }
         }
 #pragma unroll
@@ -813,29 +878,26 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
         }
       }
     }
-    if (best != kLabInf) {
-      const long long old = atomicMin(reinterpret_cast<long long*>(&S.lab[col]),
-                                      static_cast<long long>(best));
-      // a better parent alone changes nothing downstream: re-push only on
-      // a smaller (d, h)
-      if ((best & ~kParMask) < (old & ~kParMask)) S.chg[col] = 1;
-    }
+    if (col < ns) S.part[ty * ns + col] = valid ? best : kLabInf;
   }
 }
 
-// Weights of every edge into anchor-in, precomputed by its owner at the
-// start of a search: cycle graph w(u, anchor) (cheapest_pair_edge), path
-// graph the penalty difference marginal(u) - refund(anchor).
-__device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, int64_t refund_a) {
-  if (!(X.k >= X.v0 && X.k < X.v1)) return;
+// Edges into anchor-in for the running search, per owned node u (its owner
+// evaluates them when it pushes u, see collect): cycle graph w(u, anchor)
+// (cheapest_pair_edge), path graph the penalty difference marginal(u) -
+// refund(anchor), folded with the potentials: sinkc = π(u) + w - π(anchor-in).
+// π of owned nodes is fixed during a search.
+__device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, int64_t refund_a,
+                                                  int64_t pi_sink) {
   const EngineArgs& A = X.A;
-  for (int u = threadIdx.x; u < X.k; u += blockDim.x) {
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    const int u = X.v0 + i;
     int64_t w = kNoEdge;
-    if (u != anchor) {
+    if (u != anchor && u < X.k) {
       w = kind == kCycle ? pair_weight(A.M[static_cast<int64_t>(u) * A.k + anchor], has_dummy(X, u))
                          : marginal_penalty(X, u, A.load[u]) - refund_a;
     }
-    X.S.sinkw[u] = w;
+    X.S.sinkc[i] = w == kNoEdge ? kLabInf : X.S.pis[i] + w - pi_sink;
   }
 }
 
@@ -847,7 +909,7 @@ __device__ __forceinline__ void fill_sink_weights(Ctx& X, int kind, int anchor, 
 // min_open + sink_inc > S, nothing can change it or any node on its chain.
 __device__ __forceinline__ bool sink_settled(const Ctx& X, int64_t sink_inc) {
   if (sink_inc == kLabInf) return false;
-  const int64_t sl = X.S.agg->sinklab, om = X.S.agg->omin;
+  const int64_t sl = X.xslab, om = X.xomin;
   // a candidate into the sink from an open node x has (d, h) part >=
   // (d, h)(x) + sink_inc; the parent field of an equal (d, h) could still
   // lower the sink, so settle only on a strictly larger (d, h)
@@ -868,10 +930,10 @@ __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64
     relax(X, kind, anchor, refund_a, bound_mid, bound_sink);
     __syncthreads();
     PROF_MARK(X, 1);
-    collect(X, kind, anchor, true);
+    collect(X, kind, anchor, true, true);
     PROF_MARK(X, 2);
     exchange_async(X);
-    X.cur_slab = X.S.agg->sinklab;
+    X.cur_slab = X.xslab;
     advance_threshold(X);
     PROF_MARK(X, 3);
     ++rounds;
@@ -881,13 +943,14 @@ __device__ __forceinline__ int search_rounds(Ctx& X, int kind, int anchor, int64
 }
 
 __device__ __forceinline__ int64_t sink_label(const Ctx& X) {
-  return X.S.agg->sinklab;
+  return X.xslab;
 }
 
 // Start a search: labels of owned nodes to +inf, π(anchor-in) := π(anchor).
 __device__ __forceinline__ void reset_labels(Ctx& X, int64_t pi_anchor) {
   X.T = X.delta;  // labels start at the source's 0
   X.cur_slab = kLabInf;
+  if (threadIdx.x == 0) X.S.red[4] = kLabInf;  // running anchor-in candidate of this CTA
   for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
     X.S.lab[i] = kLabInf;
     X.S.chg[i] = 0;
@@ -1426,7 +1489,6 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   X.cin = inbox_cap(X.s);
   // O(k) per-search state outside shared memory (L1/L2): the weights into
   // anchor-in (read only by their owner) and each CTA's copy of the path
-  X.S.sinkw = A.colW;
   X.S.path = A.path + static_cast<int64_t>(X.rank) * (A.k + 1);
   if (A.tile_mode == 1) {
     X.wt = X.S.wt;
@@ -1436,6 +1498,10 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     X.wst = A.k;
   }
   X.par = 0;
+  X.cpar = 0;
+  X.xincl = 0;
+  X.xtotal = X.xpend = 0;
+  X.xpmin = X.xomin = X.xslab = kLabInf;
   X.err = 0;
   X.lead = X.rank == 0 && threadIdx.x == 0;
   X.n_barriers = 0;
@@ -1475,6 +1541,13 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   if (threadIdx.x < 2) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&S.rmb[threadIdx.x])),
                  "r"(X.csz));
+  }
+  if (threadIdx.x < 2 * kMaxCS) {  // cluster-window addresses of every CTA's inbox / round mbarrier
+    const int b = threadIdx.x / kMaxCS, r = threadIdx.x % kMaxCS;
+    if (r < X.csz) {
+      S.rin[threadIdx.x] = mapa_u32(smem_u32(S.inbox[b]), r);
+      S.rbar[threadIdx.x] = mapa_u32(smem_u32(&S.rmb[b]), r);
+    }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (threadIdx.x == 0) {
@@ -1617,7 +1690,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         }
       }
       if (s >= X.v0 && s < X.v1 && threadIdx.x == 0) S.lab[s - X.v0] = 0;  // the source
-      fill_sink_weights(X, kCycle, s, 0);
+      fill_sink_weights(X, kCycle, s, 0, pi_s);
       if (X.lead) {
         if (A.home[d] != -1) set_err(X, kErrAlreadyIndexed, d);
         A.home[d] = s;
@@ -1780,7 +1853,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       }
       X.delta = X.delta_path;
       reset_labels(X, pis_now);
-      fill_sink_weights(X, kPath, s, refund);
+      fill_sink_weights(X, kPath, s, refund, pis_now);
       __syncthreads();
       const int src[1] = {s};
       publish_sources(X, src, 1, kPath);

@@ -122,6 +122,7 @@ struct CS {           // shared-memory layout of one CTA
   int32_t* segmine;   // [kMaxSeg + 1] my columns per segment, then their offsets
   int32_t* segcur;    // [kMaxSeg] counting-sort cursors
   int64_t* dbg;       // [16] instrumentation counters
+  int64_t* lc;        // [16] rank 0: the lead's running EngineCtl fields (kLc*), flushed at exit
   int64_t* prof;      // [16] lead-thread cycle counters per phase
   int64_t* cw;        // [4] per-CTA profile: last exchange, work cycles, wait cycles
   uint64_t* rmb;      // [2] round mbarriers (by parity): csz arrivals + st.async bytes
@@ -152,6 +153,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.segmine = reinterpret_cast<int32_t*>(p); p += 4 * (kMaxSeg + 2);  // even: keeps 8 B alignment
   S.segcur = reinterpret_cast<int32_t*>(p); p += 4 * kMaxSeg;
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
+  S.lc = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.cw = reinterpret_cast<int64_t*>(p); p += 8 * 4;
   S.rmb = reinterpret_cast<uint64_t*>(p); p += 8 * 2;
@@ -230,6 +232,14 @@ __device__ __forceinline__ int32_t lab_h(int64_t lab) {
 }
 
 enum SearchKind : int32_t { kCycle = 0, kPath = 1, kRepair = 2 };
+
+// The lead's running counters live in rank 0's shared memory (S.lc) during a
+// launch: a global read-modify-write is a ~0.5 us round trip on the lead's
+// critical path, and every CTA waits for the lead at the next exchange.
+enum LeadCtl : int {
+  kLcDelta = 0, kLcCycleCalls, kLcPathCalls, kLcCycles, kLcPaths, kLcGain, kLcTransfers,
+  kLcChecks, kLcTbf, kLcTindex, kLcPrevSources, kLcLogN, kLcCount
+};
 
 struct Ctx {
   const EngineArgs& A;  // the __grid_constant__ kernel parameter (constant bank, no local copy)
@@ -441,20 +451,22 @@ __device__ void validate_lists(Ctx& X, int where) {
   __syncthreads();
 }
 
-// Append a home change to the move log (lead thread only).
-__device__ __forceinline__ void log_move(const EngineArgs& A, int32_t d, int32_t to) {
+// Append a home change to the move log: position `i` (the caller's count
+// S.lc[kLcLogN] + its offset), the demand onto `to`'s add list. Fire-and-
+// forget stores except the add-list counter (one atomic round trip).
+__device__ __forceinline__ void log_move(const EngineArgs& A, int64_t i, int32_t d, int32_t to) {
   if (A.log_n == nullptr) return;
-  const int32_t i = *A.log_n;
   if (i < A.log_cap) {
     A.log_d[i] = d;
     A.log_to[i] = to;
   }
-  *A.log_n = i + 1;  // past the cap: overflowed, rescans scan every demand
   if (A.add_cnt != nullptr) {  // the per-center add list of `to`
-    const int32_t c = A.add_cnt[to];
+    const int32_t c = atomicAdd(&A.add_cnt[to], 1);  // past add_cap: rescans of `to` use the move log
     if (c < A.add_cap) A.add_ids[static_cast<int64_t>(to) * A.add_cap + c] = d;
-    A.add_cnt[to] = c + 1;  // past add_cap: rescans of `to` use the move log
   }
+}
+__device__ __forceinline__ void red_add64(int64_t* p, int64_t v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
 __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
@@ -788,6 +800,35 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
   }
 }
 
+// The asral tile loop of relax: U independent (entry, key) pairs per step;
+// lim shrinks to min(lp + key * unit) over the valid entries.
+template <int U>
+__device__ __forceinline__ int64_t relax_tile(const Ctx& X, const FEntry* box, int cnt, const int16_t* wcol,
+                                              int sw, int v, int64_t lim) {
+  const int rpp = X.rpp;
+  int t = X.ty;
+  for (; t + (U - 1) * rpp < cnt; t += U * rpp) {
+    int sl[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) sl[q] = entry_slot(X, t + q * rpp);
+    int nd[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) nd[q] = box[sl[q]].nd;
+    int16_t kq[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) kq[q] = wcol[nd[q] * sw];
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (kq[q] != kNoKey16 && nd[q] != v) lim = min(lim, box[sl[q]].lp + static_cast<int64_t>(kq[q]) * kLUnit);
+  }
+  for (; t < cnt; t += rpp) {
+    const FEntry e = box[entry_slot(X, t)];
+    const int16_t key = wcol[e.nd * sw];
+    if (key != kNoKey16 && e.nd != v) lim = min(lim, e.lp + static_cast<int64_t>(key) * kLUnit);
+  }
+  return lim;
+}
+
 // Relax every edge from the sources pushed in the last exchange into this
 // CTA's nodes. bound_mid: strict upper bound on labels. Each thread owns
 // one destination column per pass and keeps its running minimum in a
@@ -823,24 +864,12 @@ __device__ __forceinline__ void relax(Ctx& X, int kind, int anchor, int64_t refu
       const int64_t lim0 = bound - base;
       int64_t lim = lim0;
       const int sw = X.wst;  // nd * wst < 2^31: 32-bit index math
-      int t = ty;
-      // four independent (entry, key) load pairs in flight per iteration
-      for (; t + 3 * rpp < cnt; t += 4 * rpp) {
-        const int s0 = entry_slot(X, t), s1 = entry_slot(X, t + rpp);
-        const int s2 = entry_slot(X, t + 2 * rpp), s3 = entry_slot(X, t + 3 * rpp);
-        const FEntry e0 = box[s0], e1 = box[s1], e2 = box[s2], e3 = box[s3];
-        const int16_t k0 = wcol[e0.nd * sw], k1 = wcol[e1.nd * sw];
-        const int16_t k2 = wcol[e2.nd * sw], k3 = wcol[e3.nd * sw];
-        if (k0 != kNoKey16 && e0.nd != v) lim = min(lim, e0.lp + static_cast<int64_t>(k0) * kUnit);
-        if (k1 != kNoKey16 && e1.nd != v) lim = min(lim, e1.lp + static_cast<int64_t>(k1) * kUnit);
-        if (k2 != kNoKey16 && e2.nd != v) lim = min(lim, e2.lp + static_cast<int64_t>(k2) * kUnit);
-        if (k3 != kNoKey16 && e3.nd != v) lim = min(lim, e3.lp + static_cast<int64_t>(k3) * kUnit);
-      }
-      for (; t < cnt; t += rpp) {
-        const FEntry e = box[entry_slot(X, t)];
-        const int16_t key = wcol[e.nd * sw];
-        if (key != kNoKey16 && e.nd != v) lim = min(lim, e.lp + static_cast<int64_t>(key) * kUnit);
-      }
+      // independent (entry, key) load pairs in flight per step: four, or
+      // eight when one thread walks the whole frontier (one row of columns,
+      // k > ~2300) through the global (L2) tile (eight measured slower at
+      // k = 2000, three rows)
+      lim = (rpp == 1 && A.tile_mode == 2) ? relax_tile<8>(X, box, cnt, wcol, sw, v, lim)
+                                           : relax_tile<4>(X, box, cnt, wcol, sw, v, lim);
       if (lim < lim0) best = lim + base;
     } else if (X.tile) {
 #pragma unroll 4
@@ -1083,80 +1112,123 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   const int k = X.k;
   const int64_t t0 = gtimer();
   // ---- T1: remove the moved demands from their old rows' lists, insert
-  // them into the new rows' lists (column owners; one thread per column, so
-  // removals precede gains) ----
+  // them into their new rows' lists. The path is simple and contiguous
+  // (edge i runs from_center(i) -> from_center(i + 1); a cycle returns to
+  // from_center(0)), so row from_center(p) loses demand(p) and gains the
+  // demand of the transfer edge that enters it: tasks (row p, column j)
+  // are independent and run in one pass, each list loaded once, the
+  // removal before the gain (as the reference's per-edge order leaves it).
   const int jlo = X.v0, jhi = min(X.v1, k);
-  for (int i = 0; i < len; ++i) {
-    const PathEdge e = S.path[i];
-    if (e.kind != kEdgeTransfer) continue;
-    for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
-      if (j == e.from_center) continue;
-      const int64_t idx = static_cast<int64_t>(e.from_center) * k + j;
-      TopK t = list_load(A, idx);
-      const int r = list_remove(t, e.demand);
-      if (r == 0) continue;
-      list_store(A, idx, t);
-      if (X.tile && (r & 1)) X.wt[static_cast<int64_t>(e.from_center) * X.wst + (j - X.v0)] = key16(t.e[0]);
-      if (r & 2) {
-        const int pos = atomicAdd(&A.inv_cnt[i], 1);
-        A.inv_cols[static_cast<int64_t>(i) * k + pos] = j;
+  const int ncol = max(0, jhi - jlo);
+  const PathEdge last = S.path[len - 1];
+  const bool extra = last.kind == kEdgeTransfer && last.to_center != S.path[0].from_center;
+  const int ntask = len + (extra ? 1 : 0);
+  for (int q = threadIdx.x; q < ntask * ncol; q += blockDim.x) {
+    const int p = q / ncol;
+    const int j = jlo + (q - p * ncol);
+    int row, rm = -1, in = -1;  // row; removal edge; gain edge
+    if (p < len) {
+      const PathEdge e = S.path[p];
+      row = e.from_center;
+      if (e.kind == kEdgeTransfer) rm = p;
+      const int pi = p > 0 ? p - 1 : len - 1;
+      const PathEdge f = S.path[pi];
+      if (f.kind == kEdgeTransfer && f.to_center == row && (p > 0 || len > 1 || pi != p)) in = pi;
+    } else {
+      row = last.to_center;
+      in = len - 1;
+    }
+    if (j == row || (rm < 0 && in < 0)) continue;
+    const int64_t idx = static_cast<int64_t>(row) * k + j;
+    int32_t din = -1, vin = 0;
+    if (in >= 0) {
+      din = S.path[in].demand;
+      const int32_t* rowin = row_of(A.rows, din);
+      vin = rowin[j] - rowin[row];
+    }
+    TopK t = list_load(A, idx);
+    bool changed = false, head = false;
+    if (rm >= 0) {
+      const int r = list_remove(t, S.path[rm].demand);
+      if (r != 0) {
+        changed = true;
+        head = (r & 1) != 0;
+        if (r & 2) {
+          const int pos = atomicAdd(&A.inv_cnt[rm], 1);
+          A.inv_cols[static_cast<int64_t>(rm) * k + pos] = j;
+        }
       }
     }
-  }
-  for (int i = 0; i < len; ++i) {
-    const PathEdge e = S.path[i];
-    if (e.kind != kEdgeTransfer) continue;
-    const int32_t* row = row_of(A.rows, e.demand);
-    const int32_t hv = row[e.to_center];
-    for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
-      if (j == e.to_center) continue;
-      const int64_t idx = static_cast<int64_t>(e.to_center) * k + j;
-      TopK t = list_load(A, idx);
-      if (list_insert(t, pack_transfer(row[j] - hv, e.demand))) {
-        if (X.tile) X.wt[static_cast<int64_t>(e.to_center) * X.wst + (j - X.v0)] = key16(t.e[0]);
-      }
-      list_store(A, idx, t);
+    if (in >= 0) {
+      changed = true;  // list_insert may clear `complete`
+      if (list_insert(t, pack_transfer(vin, din))) head = true;
     }
+    if (changed) list_store(A, idx, t);
+    if (X.tile && head) X.wt[static_cast<int64_t>(row) * X.wst + (j - X.v0)] = key16(t.e[0]);
   }
   int nd = 0;
   for (int i = 0; i < len; ++i) {
     const PathEdge e = S.path[i];
     if (e.kind == kEdgeTransfer || e.kind == kEdgeDummy) dirty[nd++] = e.to_center;
   }
-  if (X.lead) {
-    EngineCtl* ctl = A.ctl;
-    for (int i = 0; i < ctl->prev_sources; ++i) A.rowslot[A.src_list[i]] = -1;
+  // allotment bookkeeping (apply_path_edges, refine.hpp:134-164): warp 0
+  // of rank 0, one lane per path edge, so the global accesses of all edges
+  // overlap (a simple path moves distinct demands between distinct centers;
+  // load[] changes are commutative atomics; the log keeps path order)
+  if (X.rank == 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int64_t* lc = S.lc;
+    const int nprev = static_cast<int>(lc[kLcPrevSources]);
+    for (int q = lane; q < nprev; q += 32) A.rowslot[A.src_list[q]] = -1;
+    __syncwarp();
     int ns = 0;
-    for (int i = 0; i < len; ++i) {
-      const PathEdge e = S.path[i];
-      if (e.kind == kEdgeTransfer) {
-        if (A.home[e.demand] != e.from_center) { set_err(X, kErrStaleTransfer, e.demand); break; }
+    const int64_t log0 = lc[kLcLogN];
+    for (int i0 = 0; i0 < len; i0 += 32) {
+      const int i = i0 + lane;
+      PathEdge e;
+      e.kind = kEdgeNone;
+      if (i < len) e = S.path[i];
+      const bool tr = e.kind == kEdgeTransfer;
+      const unsigned bt = __ballot_sync(0xffffffffu, tr);
+      if (tr) {
+        const int32_t h = A.home[e.demand];
+        const int pos = ns + __popc(bt & ((1u << lane) - 1));
+        log_move(A, log0 + pos, e.demand, e.to_center);
+        if (h != e.from_center) set_err(X, kErrStaleTransfer, e.demand);
         A.home[e.demand] = e.to_center;
-        A.load[e.from_center] -= 1;
-        A.load[e.to_center] += 1;
+        red_add64(&A.load[e.from_center], -1);
+        red_add64(&A.load[e.to_center], 1);
         A.rowslot[e.from_center] = i;
-        A.src_list[ns++] = e.from_center;
-        ctl->transfers_applied += 1;
-        log_move(A, e.demand, e.to_center);
-      } else if (e.kind == kEdgeDummy) {
+        A.src_list[pos] = e.from_center;
+      } else if (e.kind == kEdgePenalty) {
+        if (i != len - 1) set_err(X, kErrPenaltyEdge, i);
+      }
+      ns += __popc(bt);
+    }
+    if (lane == 0) {
+      // placeholder moves (strict): in path order, a center's gain before its loss
+      for (int i = 0; i < len; ++i) {
+        const PathEdge e = S.path[i];
+        if (e.kind != kEdgeDummy) continue;
         if (A.dummies == nullptr || A.dummies[e.from_center] <= 0) {
           set_err(X, kErrPlaceholder, e.from_center);
           break;
         }
         A.dummies[e.from_center] -= 1;
         A.dummies[e.to_center] += 1;
-      } else if (e.kind == kEdgePenalty) {
-        if (i != len - 1) { set_err(X, kErrPenaltyEdge, i); break; }
       }
+      lc[kLcPrevSources] = ns;
+      lc[kLcLogN] = log0 + ns;
+      if (A.log_n != nullptr) *A.log_n = static_cast<int32_t>(log0 + ns < INT32_MAX ? log0 + ns : INT32_MAX);
+      lc[kLcTransfers] += ns;
+      int64_t r;
+      if (add_ovf(lc[kLcDelta], cost, &r)) set_err(X, kErrOverflow, 0);
+      lc[kLcDelta] = r;
+      if (add_ovf(lc[kLcGain], -cost, &r)) set_err(X, kErrOverflow, 1);
+      lc[kLcGain] = r;
+      if (kind == kCycle) lc[kLcCycles] += 1;
+      else lc[kLcPaths] += 1;
     }
-    ctl->prev_sources = ns;
-    int64_t r;
-    if (add_ovf(ctl->delta, cost, &r)) set_err(X, kErrOverflow, 0);
-    ctl->delta = r;
-    if (add_ovf(ctl->refinement_gain, -cost, &r)) set_err(X, kErrOverflow, 1);
-    ctl->refinement_gain = r;
-    if (kind == kCycle) ctl->negative_cycles_removed += 1;
-    else ctl->negative_paths_removed += 1;
   }
   if (threadIdx.x == 0) S.pub[X.par]->count = 0;
   PROF_MARK(X, 0);   // T1
@@ -1405,7 +1477,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   }
   __syncthreads();
   validate_lists(X, 2);
-  if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
+  if (X.lead) S.lc[kLcTindex] += gtimer() - t0;
   return nd;
 }
 
@@ -1414,7 +1486,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
 __device__ __forceinline__ void certify(Ctx& X) {
   const EngineArgs& A = X.A;
   if (!A.check_invariants) return;
-  if (X.lead) A.ctl->invariant_checks += 1;
+  if (X.lead) X.S.lc[kLcChecks] += 1;
   bool bad = false;
   for (int u = 0; u < X.k; ++u) {
     const int64_t piu = pi_of(X, u);
@@ -1459,8 +1531,8 @@ __device__ __forceinline__ void check_path_sum(Ctx& X, int kind, int anchor, int
 
 __device__ __forceinline__ void add_delta(Ctx& X, int64_t v, int arg) {
   int64_t r;
-  if (add_ovf(X.A.ctl->delta, v, &r)) set_err(X, kErrOverflow, arg);
-  X.A.ctl->delta = r;
+  if (add_ovf(X.S.lc[kLcDelta], v, &r)) set_err(X, kErrOverflow, arg);
+  X.S.lc[kLcDelta] = r;
 }
 
 }  // namespace cl
@@ -1515,6 +1587,21 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   X.cur_slab = kLabInf;
   X.dbg = X.S.dbg;
   if (threadIdx.x < 16) X.dbg[threadIdx.x] = 0;
+  if (X.rank == 0 && threadIdx.x == 0) {
+    const EngineCtl* ctl = A.ctl;
+    X.S.lc[kLcDelta] = ctl->delta;
+    X.S.lc[kLcCycleCalls] = ctl->cycle_refine_calls;
+    X.S.lc[kLcPathCalls] = ctl->path_refine_calls;
+    X.S.lc[kLcCycles] = ctl->negative_cycles_removed;
+    X.S.lc[kLcPaths] = ctl->negative_paths_removed;
+    X.S.lc[kLcGain] = ctl->refinement_gain;
+    X.S.lc[kLcTransfers] = ctl->transfers_applied;
+    X.S.lc[kLcChecks] = ctl->invariant_checks;
+    X.S.lc[kLcTbf] = ctl->t_bf_ns;
+    X.S.lc[kLcTindex] = ctl->t_index_ns;
+    X.S.lc[kLcPrevSources] = ctl->prev_sources;
+    X.S.lc[kLcLogN] = A.log_n != nullptr ? *A.log_n : 0;
+  }
   if (threadIdx.x < 16) X.S.prof[threadIdx.x] = 0;
   if (threadIdx.x < 4) X.S.cw[threadIdx.x] = threadIdx.x == 0 ? clock64() : 0;
   CS& S = X.S;
@@ -1692,18 +1779,22 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       if (s >= X.v0 && s < X.v1 && threadIdx.x == 0) S.lab[s - X.v0] = 0;  // the source
       fill_sink_weights(X, kCycle, s, 0, pi_s);
       if (X.lead) {
-        if (A.home[d] != -1) set_err(X, kErrAlreadyIndexed, d);
+        const int32_t h = A.home[d];
+        const int64_t li = S.lc[kLcLogN];
+        log_move(A, li, d, s);
+        if (h != -1) set_err(X, kErrAlreadyIndexed, d);
         A.home[d] = s;
-        A.load[s] += 1;
-        log_move(A, d, s);
+        red_add64(&A.load[s], 1);
+        S.lc[kLcLogN] = li + 1;
+        if (A.log_n != nullptr) *A.log_n = static_cast<int32_t>(li + 1 < INT32_MAX ? li + 1 : INT32_MAX);
         if (strict) add_delta(X, cost, d);
-        A.ctl->cycle_refine_calls += 1;
+        S.lc[kLcCycleCalls] += 1;
       }
       __syncthreads();
       collect(X, kCycle, s);
       exchange(X);
       validate_lists(X, 1);
-      if (X.lead) A.ctl->t_index_ns += gtimer() - t0;
+      if (X.lead) S.lc[kLcTindex] += gtimer() - t0;
       PROF_MARK(X, 4);  // insert round
       kind = kCycle;
       refund = 0;
@@ -1730,7 +1821,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         stage = after;
         continue;
       }
-      if (X.lead) X.A.ctl->t_bf_ns += gtimer() - t_search;
+      if (X.lead) X.S.lc[kLcTbf] += gtimer() - t_search;
       const int64_t sl = sink_label(X);
       const bool found = !X.err && sl != kLabInf && lab_d(sl) < 0;
       if (!found) {
@@ -1816,7 +1907,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     }
 
     if (stage == kStPathBound) {
-      if (X.lead) A.ctl->path_refine_calls += 1;
+      if (X.lead) S.lc[kLcPathCalls] += 1;
       refund = refund_penalty(X, s, A.load[s]);
       // C = min_{u != s} marginal(u) - refund + π(u) - π(s): the most a
       // penalty edge can subtract; prune the search to d_rc < -C
@@ -1874,6 +1965,18 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     stage = (A.fixpoint && applied && A.load[s] > cap) ? kStPathBound : kStArrival;
   }
   if (X.lead) {
+    EngineCtl* ctl = A.ctl;
+    ctl->delta = S.lc[kLcDelta];
+    ctl->cycle_refine_calls = S.lc[kLcCycleCalls];
+    ctl->path_refine_calls = S.lc[kLcPathCalls];
+    ctl->negative_cycles_removed = S.lc[kLcCycles];
+    ctl->negative_paths_removed = S.lc[kLcPaths];
+    ctl->refinement_gain = S.lc[kLcGain];
+    ctl->transfers_applied = S.lc[kLcTransfers];
+    ctl->invariant_checks = S.lc[kLcChecks];
+    ctl->t_bf_ns = S.lc[kLcTbf];
+    ctl->t_index_ns = S.lc[kLcTindex];
+    ctl->prev_sources = static_cast<int32_t>(S.lc[kLcPrevSources]);
     for (int i = 0; i < 15; ++i) A.ctl->prof[i] += S.prof[i];  // cycles per phase
     for (int i = 0; i < 16; ++i) A.ctl->dbg[i] += X.dbg[i];
     A.ctl->barriers += X.n_barriers;

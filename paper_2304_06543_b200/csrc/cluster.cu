@@ -1454,10 +1454,12 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       __syncthreads();
     }
   }
-  if (threadIdx.x == 0) S.pub[X.par]->count = 0;
-  PROF_MARK(X, 13);  // T3
-  exchange(X);
-  PROF_MARK(X, 12);
+  if (total > 0) {  // uniform: every CTA read the same counters after the T1 exchange
+    if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+    PROF_MARK(X, 13);  // T3
+    exchange(X);       // orders the rescanned lists before their readers
+    PROF_MARK(X, 12);
+  }
   // rescanned entries now hold the (up to) four smallest transfers of their
   // row: complete when fewer than four exist; refresh my tile columns
   for (int i = 0; i < len; ++i) {
@@ -1910,21 +1912,36 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       if (X.lead) S.lc[kLcPathCalls] += 1;
       refund = refund_penalty(X, s, A.load[s]);
       // C = min_{u != s} marginal(u) - refund + π(u) - π(s): the most a
-      // penalty edge can subtract; prune the search to d_rc < -C
+      // penalty edge can subtract; prune the search to d_rc < -C. One
+      // exchange carries C and the search's source: the labels are reset
+      // and s is published before it (discarded when the bound prunes), and
+      // the penalty edges into anchor-in are evaluated in the same pass.
       const int64_t pis_now = pi_of(X, s);
-      int64_t lmin = kEmpty;
-      for (int u = X.v0 + threadIdx.x; u < min(X.v1, k); u += blockDim.x) {
-        if (u == s) continue;
-        lmin = min(lmin, marginal_penalty(X, u, A.load[u]) - refund + S.pis[u - X.v0]);
+      X.delta = X.delta_path;
+      reset_labels(X, pis_now);
+      long long lmin = kEmpty;
+      for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+        const int u = X.v0 + i;
+        int64_t sc = kLabInf;
+        if (u != s && u < k) {
+          const int64_t w = marginal_penalty(X, u, A.load[u]) - refund;
+          lmin = min(lmin, static_cast<long long>(w + S.pis[i]));
+          sc = S.pis[i] + w - pis_now;
+        }
+        S.sinkc[i] = sc;
       }
-      if (threadIdx.x == 0) S.red[0] = kEmpty;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+      if ((threadIdx.x & 31) == 0) S.wred[threadIdx.x >> 5] = lmin;
       __syncthreads();
-      atomicMin(reinterpret_cast<long long*>(&S.red[0]), static_cast<long long>(lmin));
-      __syncthreads();
+      const int src[1] = {s};
+      publish_sources(X, src, 1, kPath);
       if (threadIdx.x == 0) {
-        S.pub[X.par]->val = S.red[0];
-        S.pub[X.par]->count = 0;
+        long long m = kEmpty;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = min(m, static_cast<long long>(S.wred[w]));
+        S.pub[X.par]->val = m;
       }
+      __syncthreads();
       exchange(X);
       PROF_MARK(X, 7);  // path bound
       int64_t cmin = kEmpty;
@@ -1942,14 +1959,6 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         X.dbg[14] = max(X.dbg[14], -C);
         X.dbg[15] += refund;
       }
-      X.delta = X.delta_path;
-      reset_labels(X, pis_now);
-      fill_sink_weights(X, kPath, s, refund, pis_now);
-      __syncthreads();
-      const int src[1] = {s};
-      publish_sources(X, src, 1, kPath);
-      __syncthreads();
-      exchange(X);
       kind = kPath;
       bound = (-C) * kLUnit;
       X.prune = true;

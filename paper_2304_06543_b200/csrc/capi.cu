@@ -764,7 +764,7 @@ size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
   return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * cin + 2 * sizeof(cl::Pub) + 8 * 16 +
          2 * sizeof(cl::Pub) * cl::kMaxCS + 4 * 3 * cl::kMaxSeg +
          4 * 2 * cl::kMaxMine + 4 * (2 * cl::kMaxSeg + 2) +
-         8 * 16 + 8 * 16 + 8 * 16 + 8 * 4 + 8 * 2 +
+         8 * 16 + 8 * 16 + 8 * 16 + 8 * 8 + 8 * 4 + 8 * 2 +
          12 * block + 4 * 16 +
          4 * static_cast<size_t>(cl::kRowSlots) * ((k + 31) / 32) +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16 +

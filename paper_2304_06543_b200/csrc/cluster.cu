@@ -122,6 +122,7 @@ struct CS {           // shared-memory layout of one CTA
   int32_t* segmine;   // [kMaxSeg + 1] my columns per segment, then their offsets
   int32_t* segcur;    // [kMaxSeg] counting-sort cursors
   int64_t* dbg;       // [16] instrumentation counters
+  int64_t* cred;      // [2][4] collect's reductions by parity: pmin, omin, sink candidate
   int64_t* lc;        // [16] rank 0: the lead's running EngineCtl fields (kLc*), flushed at exit
   int64_t* prof;      // [16] lead-thread cycle counters per phase
   int64_t* cw;        // [4] per-CTA profile: last exchange, work cycles, wait cycles
@@ -154,6 +155,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.segcur = reinterpret_cast<int32_t*>(p); p += 4 * kMaxSeg;
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.lc = reinterpret_cast<int64_t*>(p); p += 8 * 16;
+  S.cred = reinterpret_cast<int64_t*>(p); p += 8 * 8;
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.cw = reinterpret_cast<int64_t*>(p); p += 8 * 4;
   S.rmb = reinterpret_cast<uint64_t*>(p); p += 8 * 2;
@@ -671,7 +673,14 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
   // whose own counter every thread read before the CTA barrier that
   // separates the two calls); the other parity is reset for the next call
   int* slots = &S.misc[8 + X.cpar];
-  if (threadIdx.x == 0) S.misc[8 + (X.cpar ^ 1)] = 0;
+  int* heldc = &S.misc[12 + X.cpar];
+  int64_t* cr = S.cred + 4 * X.cpar;
+  if (threadIdx.x == 0) {  // the other parity, for the next call
+    S.misc[8 + (X.cpar ^ 1)] = 0;
+    S.misc[12 + (X.cpar ^ 1)] = 0;
+    int64_t* cn = S.cred + 4 * (X.cpar ^ 1);
+    cn[0] = cn[1] = cn[2] = kLabInf;
+  }
   X.cpar ^= 1;
   const int ns = X.v1 - X.v0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -741,58 +750,38 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
       }
     }
   }
-  if (warp < nwa) {
-    // most rounds change few nodes: reduce only what is there
-    if (__any_sync(0xffffffffu, held != 0)) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
-        held += __shfl_xor_sync(0xffffffffu, held, o);
-      }
-    }
-    if (__any_sync(0xffffffffu, omin != kLabInf)) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
-    }
-    if (__any_sync(0xffffffffu, smin != kLabInf)) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
-    }
-    if (lane == 0) {
-      S.wred[warp] = pmin;
-      S.wred[32 + warp] = omin;
-      S.wred[64 + warp] = smin;
-      S.wred[96 + warp] = held;
-    }
+  // few threads hold values: shared-memory atomics (64-bit min is a CAS
+  // loop, cheap without contention) instead of warp reductions
+  if (held) {
+    atomicAdd(heldc, held);
+    atomicMin(reinterpret_cast<long long*>(&cr[0]), pmin);
   }
+  if (omin != kLabInf) atomicMin(reinterpret_cast<long long*>(&cr[1]), omin);
+  if (smin != kLabInf) atomicMin(reinterpret_cast<long long*>(&cr[2]), smin);
   __syncthreads();
   const int cnt = min(*slots, X.cin);
   if (async && cnt > 0) {
-    // (entry, destination) pairs over the CTA; this CTA's own copy is local
-    const int nd = X.csz - 1;
-    const unsigned off0 = static_cast<unsigned>(sizeof(FEntry)) * (X.rank * X.cin);
-    for (int q = threadIdx.x; q < cnt * nd; q += blockDim.x) {
-      const int e = q / nd, rr = q - e * nd;
-      const int r = rr < X.rank ? rr : rr + 1;
-      const unsigned off = off0 + static_cast<unsigned>(sizeof(FEntry)) * e;
-      const int4 v = *reinterpret_cast<const int4*>(&S.inbox[X.par][X.rank * X.cin + e]);
-      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
-                   ::"r"(S.rin[X.par * kMaxCS + r] + off), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w),
-                   "r"(S.rbar[X.par * kMaxCS + r]) : "memory");
+    // (entry, destination) pairs over the CTA: thread -> destination
+    // threadIdx % 16, entries threadIdx / 16 + j * blockDim / 16; this CTA's
+    // own copy is local
+    const int r = threadIdx.x & (kMaxCS - 1);
+    if (r < X.csz && r != X.rank) {
+      const unsigned rin = S.rin[X.par * kMaxCS + r] + static_cast<unsigned>(sizeof(FEntry)) * (X.rank * X.cin);
+      const unsigned rbar = S.rbar[X.par * kMaxCS + r];
+      const FEntry* mine = &S.inbox[X.par][X.rank * X.cin];
+      for (int e = threadIdx.x / kMaxCS; e < cnt; e += blockDim.x / kMaxCS) {
+        const int4 v = *reinterpret_cast<const int4*>(&mine[e]);
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                     ::"r"(rin + static_cast<unsigned>(sizeof(FEntry)) * e), "r"(v.x), "r"(v.y), "r"(v.z),
+                     "r"(v.w), "r"(rbar) : "memory");
+      }
     }
   }
   if (threadIdx.x == 0) {
-    long long pm = kLabInf, om = kLabInf, sm = kLabInf;
-    int hd = 0;
-    for (int w = 0; w < nwa; ++w) {
-      pm = min(pm, static_cast<long long>(S.wred[w]));
-      om = min(om, static_cast<long long>(S.wred[32 + w]));
-      sm = min(sm, static_cast<long long>(S.wred[64 + w]));
-      hd += static_cast<int>(S.wred[96 + w]);
-    }
+    const int64_t pm = cr[0], om = cr[1], sm = cr[2];
     Pub* p = S.pub[X.par];
     p->count = cnt;
-    p->pending = hd;
+    p->pending = *heldc;
     p->pmin = pm;
     p->omin = min(pm, om);
     if (sm < S.red[4]) S.red[4] = sm;
@@ -1626,6 +1615,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     }
   }
   if (threadIdx.x < 16) S.misc[threadIdx.x] = 0;
+  if (threadIdx.x < 8) S.cred[threadIdx.x] = kLabInf;
   X.rph = 0;
   if (threadIdx.x < 2) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&S.rmb[threadIdx.x])),

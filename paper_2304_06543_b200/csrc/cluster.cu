@@ -581,12 +581,15 @@ __device__ __forceinline__ void exchange_async(Ctx& X) {
 __device__ __forceinline__ void exchange_finish(Ctx& X) {
   CS& S = X.S;
   S.all = S.allb[X.par];
-  // every warp reduces the CTAs' pubs itself (identical results everywhere)
-  const int lane = threadIdx.x & 31;
+  // every warp reduces the CTAs' pubs itself (identical results
+  // everywhere); both half-warps hold all csz <= 16 pubs, so four shuffle
+  // levels leave every lane with the result
+  static_assert(kMaxCS == 16, "half-warp reductions");
+  const int lane = threadIdx.x & 31, hl = lane & 15;
   int c = 0, e = 0, pend = 0;
   long long pmin = kLabInf, omin = kLabInf, slab = kLabInf;
-  if (lane < X.csz) {
-    const Pub& p = S.all[lane];
+  if (hl < X.csz) {
+    const Pub& p = S.all[hl];
     c = (p.count >= 0 && p.count <= X.cin) ? p.count : 0;
     e = p.err;
     pend = p.pending;
@@ -596,19 +599,24 @@ __device__ __forceinline__ void exchange_finish(Ctx& X) {
   }
   int incl = c;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < 16; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+    if (hl >= o) incl += y;
   }
-  X.xincl = incl;
-  X.xtotal = __shfl_sync(0xffffffffu, incl, 31);
+  X.xincl = incl;  // lanes < csz (entry_slot); lane 15: the total
+  X.xtotal = __shfl_sync(0xffffffffu, incl, 15);
   if (__any_sync(0xffffffffu, e != 0)) X.err = 1;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 8; o > 0; o >>= 1) {
     pend += __shfl_xor_sync(0xffffffffu, pend, o);
-    pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
     omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
     slab = min(slab, __shfl_xor_sync(0xffffffffu, slab, o));
+  }
+  if (pend != 0) {  // warp-uniform; held-back minimum only when something is held
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+  } else {
+    pmin = kLabInf;
   }
   X.xpend = pend;
   X.xpmin = pmin;

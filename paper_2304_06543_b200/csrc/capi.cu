@@ -139,7 +139,7 @@ struct lbdd_b200_instance {
   // scan results
   bool scanned = false;
   int64_t min_cost = 0, max_cost = 0;
-  DevBuf<int32_t> best_center;
+  DevBuf<int32_t> best_center, arr_s;
   DevBuf<int64_t> keys, keys_sorted, minmax;
   DevBuf<unsigned char> cub_tmp;
 
@@ -177,7 +177,7 @@ struct lbdd_b200_instance {
                     static_cast<void*>(d_par)}) {
       if (p) cudaFree(p);
     }
-    best_center.release(); keys.release(); keys_sorted.release(); minmax.release();
+    best_center.release(); arr_s.release(); keys.release(); keys_sorted.release(); minmax.release();
     cub_tmp.release(); home.release(); order.release(); rowslot.release(); src_list.release();
     inv_cnt.release(); inv_cols.release();
     for (int s = 0; s < 2; ++s) {
@@ -764,7 +764,8 @@ size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
   return 8 * s + 8 * s + 2 * sizeof(cl::FEntry) * cl::kMaxCS * cin + 2 * sizeof(cl::Pub) + 8 * 16 +
          2 * sizeof(cl::Pub) * cl::kMaxCS + 4 * 3 * cl::kMaxSeg +
          4 * 2 * cl::kMaxMine + 4 * (2 * cl::kMaxSeg + 2) +
-         8 * 16 + 8 * 16 + 8 * 16 + 8 * 8 + 8 * 4 + 8 * 2 +
+         8 * 16 + 8 * 16 + 8 * 16 + 8 * 8 + 8 * 4 + 4 * 4 + 4 * 2 * static_cast<size_t>(s + 1) + 8 +
+         8 * 4 + 8 * 2 +
          12 * block + 4 * 16 +
          4 * static_cast<size_t>(cl::kRowSlots) * ((k + 31) / 32) +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16 +
@@ -976,6 +977,12 @@ void solve_asral(lbdd_b200_instance* I, const lbdd_solver_options* o, int32_t so
   A.mode = 0;
   A.arr_keys = I->keys_sorted.p;
   A.best_center = I->best_center.p;
+  I->arr_s.ensure(I->n);
+  g_launches++;
+  arrival_centers_kernel<<<grid_for(I->n), 256, 0, I->stream>>>(I->keys_sorted.p, I->best_center.p, I->n,
+                                                              I->arr_s.p);
+  CUDA_OK(cudaGetLastError());
+  A.arr_s = I->arr_s.p;
   A.fixpoint = o && o->refine_to_fixpoint;
   A.check_invariants = o && o->check_invariants;
   const int64_t a_end = arrivals < 0 ? I->n : std::min<int64_t>(arrivals, I->n);

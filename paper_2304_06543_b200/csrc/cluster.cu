@@ -123,6 +123,9 @@ struct CS {           // shared-memory layout of one CTA
   int32_t* segcur;    // [kMaxSeg] counting-sort cursors
   int64_t* dbg;       // [16] instrumentation counters
   int64_t* cred;      // [2][4] collect's reductions by parity: pmin, omin, sink candidate
+  int64_t* pkey;      // [4] asral prefetch ring (arrival a at a & 3): sorted key (cost << 32 | d)
+  int32_t* ps;        // [4] ... and its center
+  int32_t* prow;      // [2][s + 1] cost row of arrival a (at a & 1): my columns, then CM[d][s] at [s]
   int64_t* lc;        // [16] rank 0: the lead's running EngineCtl fields (kLc*), flushed at exit
   int64_t* prof;      // [16] lead-thread cycle counters per phase
   int64_t* cw;        // [4] per-CTA profile: last exchange, work cycles, wait cycles
@@ -156,6 +159,10 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.dbg = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.lc = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.cred = reinterpret_cast<int64_t*>(p); p += 8 * 8;
+  S.pkey = reinterpret_cast<int64_t*>(p); p += 8 * 4;
+  S.ps = reinterpret_cast<int32_t*>(p); p += 4 * 4;
+  S.prow = reinterpret_cast<int32_t*>(p); p += 4 * 2 * static_cast<size_t>(s + 1);
+  p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
   S.prof = reinterpret_cast<int64_t*>(p); p += 8 * 16;
   S.cw = reinterpret_cast<int64_t*>(p); p += 8 * 4;
   S.rmb = reinterpret_cast<uint64_t*>(p); p += 8 * 2;
@@ -470,6 +477,21 @@ __device__ __forceinline__ void log_move(const EngineArgs& A, int64_t i, int32_t
 __device__ __forceinline__ void red_add64(int64_t* p, int64_t v) {
   atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
+
+// ---- asral arrival prefetch (cp.async: no thread waits on the loads) ----
+// The arrival order is fixed, so arrival a + 2's (key, center) and arrival
+// a + 1's cost row (this CTA's columns + CM[d][s]) are copied into shared
+// memory while arrival a runs: the insert then starts from shared memory
+// instead of a key -> center -> cost-row chain of dependent global loads.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ bool has_dummy(const Ctx& X, int u) {
   return X.A.dummies != nullptr && X.A.dummies[u] > 0;
@@ -1534,6 +1556,25 @@ __device__ __forceinline__ void add_delta(Ctx& X, int64_t v, int arg) {
   X.S.lc[kLcDelta] = r;
 }
 
+__device__ __forceinline__ void prefetch_scalars(Ctx& X, int64_t a) {
+  if (threadIdx.x == 0 && a < X.A.a_end) {
+    cp_async8(&X.S.pkey[a & 3], &X.A.arr_keys[a]);
+    cp_async4(&X.S.ps[a & 3], &X.A.arr_s[a]);
+  }
+}
+// needs arrival a's scalars landed and visible (wait + CTA barrier)
+__device__ __forceinline__ void prefetch_row(Ctx& X, int64_t a) {
+  if (a >= X.A.a_end) return;
+  const int32_t d = static_cast<int32_t>(X.S.pkey[a & 3] & 0xffffffffLL);
+  const int32_t s = X.S.ps[a & 3];
+  const int32_t* row = row_of(X.A.rows, d);
+  int32_t* dst = X.S.prow + (a & 1) * (X.s + 1);
+  for (int i = threadIdx.x; i < X.v1 - X.v0; i += blockDim.x) {
+    if (X.v0 + i < X.k) cp_async4(&dst[i], &row[X.v0 + i]);
+  }
+  if (threadIdx.x == blockDim.x - 1) cp_async4(&dst[X.s], &row[s]);
+}
+
 }  // namespace cl
 
 // Shared memory: see cl::carve.
@@ -1674,6 +1715,14 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
     __syncthreads();
   }
   int* dirty = dirty_buf + X.rank * (2 * k + 4);  // per-CTA scratch
+  const bool pf = !strict && A.arr_s != nullptr;  // asral arrival prefetch
+  if (pf) {
+    prefetch_scalars(X, A.a_begin);
+    prefetch_scalars(X, A.a_begin + 1);
+    cp_async_wait_all();
+    __syncthreads();
+    prefetch_row(X, A.a_begin);
+  }
 
   PROF_MARK(X, 14);
   // The arrival loop as a state machine: every phase -- above all the search
@@ -1705,7 +1754,16 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       }
       const int64_t t0 = gtimer();
       int dum_a = 0;  // placeholder at the anchor after the eviction (strict)
-      if (!strict) {
+      if (pf) {
+        cp_async_wait_all();  // arrival a's (and a + 1's) scalars, a's cost row
+        __syncthreads();
+        const int64_t key = S.pkey[a & 3];
+        d = static_cast<int32_t>(key & 0xffffffffLL);
+        cost = key >> 32;
+        s = S.ps[a & 3];
+        prefetch_scalars(X, a + 2);
+        prefetch_row(X, a + 1);
+      } else if (!strict) {
         const int64_t key = A.arr_keys[a];
         d = static_cast<int32_t>(key & 0xffffffffLL);
         cost = key >> 32;
@@ -1756,12 +1814,14 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       reset_labels(X, pi_s);
       __syncthreads();
       const int32_t* row = row_of(A.rows, d);
-      const int32_t hv = row[s];
+      const int32_t* prow = S.prow + ((a - 1) & 1) * (X.s + 1);  // arrival a - 1 (a was advanced)
+      const int32_t hv = pf ? prow[X.s] : row[s];
       for (int j = X.v0 + threadIdx.x; j < min(X.v1, k); j += blockDim.x) {
         if (j == s) continue;
         const int64_t idx = static_cast<int64_t>(s) * k + j;
         TopK t = list_load(A, idx);
-        if (list_insert(t, pack_transfer(row[j] - hv, d))) {
+        const int32_t cj = pf ? prow[j - X.v0] : row[j];
+        if (list_insert(t, pack_transfer(cj - hv, d))) {
           if (X.tile) X.wt[static_cast<int64_t>(s) * X.wst + (j - X.v0)] = key16(t.e[0]);
         }
         list_store(A, idx, t);
@@ -1827,7 +1887,10 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       if (!found) {
         if (kind == kCycle) {
           PROF_MARK(X, 5);  // cycle search
-          apply_repair(X);  // π += min(0, d) over the explored region
+          // π += min(0, d) over the explored region; a search that never ran
+          // a round labelled nothing but its source (d = 0): π is unchanged
+          // and needs no cluster barrier (uniform: every CTA counted the same)
+          if (rounds > 0) apply_repair(X);
           __syncthreads();
           PROF_MARK(X, 6);
           certify(X);

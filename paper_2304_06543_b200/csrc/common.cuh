@@ -156,6 +156,7 @@ struct EngineArgs {
   // arrivals
   const int64_t* arr_keys;    // asral: sorted (cost << 32 | d)
   const int32_t* best_center; // asral: row argmin center
+  const int32_t* arr_s;       // asral: best_center of the a-th arrival (gathered once per solve)
   const int32_t* order;       // strict: processing order (nullptr = identity)
   int64_t a_begin;
   int64_t a_end;

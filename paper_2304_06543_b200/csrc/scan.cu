@@ -251,6 +251,16 @@ __global__ void piece_count_kernel(const int32_t* __restrict__ cnt, int32_t k, i
   }
 }
 
+// Arrival-ordered centers (asral): arr_s[a] = best_center[d(a)], so the
+// engine reads an arrival's (cost, demand) and center without a dependent
+// gather and can prefetch them ahead.
+__global__ void arrival_centers_kernel(const int64_t* __restrict__ keys, const int32_t* __restrict__ best,
+                                       int64_t n, int32_t* __restrict__ arr_s) {
+  for (int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; a < n;
+       a += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    arr_s[a] = best[keys[a] & 0xffffffffLL];
+}
+
 __global__ void fill_i64_kernel(int64_t* p, int64_t count, int64_t v) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {

@@ -53,7 +53,10 @@ constexpr int kMaxMine = 1024;
 // changed nodes past it stay pending for a later round -- the Δ-stepping
 // hold-back mechanism -- so shared memory no longer grows with k
 constexpr int kInCap = 128;
-__host__ __device__ inline int inbox_cap(int s) { return s < kInCap ? s : kInCap; }         // invalidated (segment, column) pairs a CTA owns per rescan
+// past s = 128 (k > ~2000) the cap drops to 96 so that the engine's shared
+// memory stays under the 100 KB carve-out step (k = 5000: 98.5 KB) and the
+// SM keeps its larger L1 for the global key tile (measured 11% at k = 5000)
+__host__ __device__ inline int inbox_cap(int s) { return s <= kInCap ? s : 96; }         // invalidated (segment, column) pairs a CTA owns per rescan
 
 // A frontier entry as pushed into every CTA's inbox: the node (bit 31: a
 // surplus placeholder sits there, strict-mode edge rule) and its label with
@@ -687,6 +690,20 @@ __device__ __forceinline__ void push_entry(Ctx& X, int pos, int v, int64_t label
   }
 }
 
+// CTA-wide min into a shared slot from the lanes with `has` (whole warp calls)
+__device__ __forceinline__ void cta_min(bool has, long long v, int64_t* slot) {
+  const unsigned bal = __ballot_sync(0xffffffffu, has);
+  if (bal == 0) return;
+  if (__popc(bal) <= 2) {
+    if (has) atomicMin(reinterpret_cast<long long*>(slot), v);
+    return;
+  }
+  if (!has) v = kLabInf;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(reinterpret_cast<long long*>(slot), v);
+}
+
 // Δ-stepping: only improved nodes with label <= X.T are pushed; the rest
 // stay pending (their flag kept) and report their count and minimum.
 // merge: fold the relax partials of this round into the labels first (the
@@ -780,14 +797,26 @@ __device__ __forceinline__ void collect(Ctx& X, int kind, int anchor, bool async
       }
     }
   }
-  // few threads hold values: shared-memory atomics (64-bit min is a CAS
-  // loop, cheap without contention) instead of warp reductions
-  if (held) {
-    atomicAdd(heldc, held);
-    atomicMin(reinterpret_cast<long long*>(&cr[0]), pmin);
+  // shared-memory atomics for the CTA minima (a 64-bit min is a CAS loop:
+  // cheap while few lanes contend); a warp with more than two values
+  // reduces them with shuffles first (k = 5000: ~10 warps hold nodes)
+  if (nwa <= 2) {  // k <= ~2000: few values per warp, plain atomics
+    if (held) {
+      atomicAdd(heldc, held);
+      atomicMin(reinterpret_cast<long long*>(&cr[0]), pmin);
+    }
+    if (omin != kLabInf) atomicMin(reinterpret_cast<long long*>(&cr[1]), omin);
+    if (smin != kLabInf) atomicMin(reinterpret_cast<long long*>(&cr[2]), smin);
+  } else if (warp < nwa) {
+    cta_min(held != 0, pmin, &cr[0]);
+    cta_min(omin != kLabInf, omin, &cr[1]);
+    cta_min(smin != kLabInf, smin, &cr[2]);
+    if (__any_sync(0xffffffffu, held != 0)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) held += __shfl_xor_sync(0xffffffffu, held, o);
+      if (lane == 0) atomicAdd(heldc, held);
+    }
   }
-  if (omin != kLabInf) atomicMin(reinterpret_cast<long long*>(&cr[1]), omin);
-  if (smin != kLabInf) atomicMin(reinterpret_cast<long long*>(&cr[2]), smin);
   __syncthreads();
   const int cnt = min(*slots, X.cin);
   if (async && cnt > 0) {

@@ -327,7 +327,9 @@ __device__ __forceinline__ int64_t refund_penalty(Ctx& X, int s, int64_t load) {
 
 // ---- per-entry top-4 lists: the 4 smallest (key, demand) of a heap ----
 // Entry (u, j) keeps its minimum in M[u*k+j] (what every reader uses) and
-// up to three successors in MX[(u*k+j)*3 ..]; LN[u*k+j] = length | complete
+// up to three successors in MX (three k*k planes, slot i at i*k*k + u*k+j:
+// a warp's 32 consecutive lists load as three coalesced 256 B rows, not a
+// 768 B strided span per slot); LN[u*k+j] = length | complete
 // << 3, where "complete" means the list holds every demand sitting at u.
 // Invariant: the list is exactly the `length` smallest transfers of the
 // heap (subspace.hpp:26-231), so removing the head promotes the true next
@@ -338,13 +340,15 @@ struct TopK {
   int len;
   bool complete;
 };
+__device__ __forceinline__ int64_t* mx_slot(const EngineArgs& A, int64_t idx, int i) {
+  return A.MX + static_cast<int64_t>(i) * A.k * A.k + idx;
+}
 __device__ __forceinline__ TopK list_load(const EngineArgs& A, int64_t idx) {
   TopK t;
   t.e[0] = A.M[idx];
-  const int64_t* mx = A.MX + idx * 3;
-  t.e[1] = mx[0];
-  t.e[2] = mx[1];
-  t.e[3] = mx[2];
+  t.e[1] = *mx_slot(A, idx, 0);
+  t.e[2] = *mx_slot(A, idx, 1);
+  t.e[3] = *mx_slot(A, idx, 2);
   const uint8_t ln = A.LN[idx];
   t.len = ln & 7;
   t.complete = (ln & 8) != 0;
@@ -352,10 +356,9 @@ __device__ __forceinline__ TopK list_load(const EngineArgs& A, int64_t idx) {
 }
 __device__ __forceinline__ void list_store(const EngineArgs& A, int64_t idx, const TopK& t) {
   A.M[idx] = t.e[0];
-  int64_t* mx = A.MX + idx * 3;
-  mx[0] = t.e[1];
-  mx[1] = t.e[2];
-  mx[2] = t.e[3];
+  *mx_slot(A, idx, 0) = t.e[1];
+  *mx_slot(A, idx, 1) = t.e[2];
+  *mx_slot(A, idx, 2) = t.e[3];
   A.LN[idx] = static_cast<uint8_t>(t.len | (t.complete ? 8 : 0));
 }
 // returns true when the head changed
@@ -383,13 +386,12 @@ __device__ __forceinline__ bool list_insert(TopK& t, int64_t v) {
 // the four smallest; the prefilter reads slot 3 at L2 (a stale larger value
 // only costs the cascade).
 __device__ __forceinline__ void list_sink(const EngineArgs& A, int64_t idx, int64_t x) {
-  int64_t* mx = A.MX + idx * 3;
-  if (x >= static_cast<int64_t>(__ldcg(reinterpret_cast<const long long*>(mx + 2)))) return;
+  if (x >= static_cast<int64_t>(__ldcg(reinterpret_cast<const long long*>(mx_slot(A, idx, 2))))) return;
   int64_t old = atomicMin(reinterpret_cast<long long*>(&A.M[idx]), static_cast<long long>(x));
   if (old == x) return;
   x = max(old, x);
   for (int i = 0; i < kTopK - 1 && x != kEmpty; ++i) {
-    old = atomicMin(reinterpret_cast<long long*>(&mx[i]), static_cast<long long>(x));
+    old = atomicMin(reinterpret_cast<long long*>(mx_slot(A, idx, i)), static_cast<long long>(x));
     if (old == x) return;
     x = max(old, x);
   }
@@ -1154,7 +1156,7 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
 // invalidate and fold gains for their columns; the lead updates the
 // allotment; all CTAs rescan the invalidated entries over the final
 // buckets. Fills `dirty` with the rows whose out-edges may now violate π.
-__device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, int* dirty) {
+__device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, int* dirty, int anchor) {
   CS& S = X.S;
   const EngineArgs& A = X.A;
   const int k = X.k;
@@ -1219,6 +1221,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     const PathEdge e = S.path[i];
     if (e.kind == kEdgeTransfer || e.kind == kEdgeDummy) dirty[nd++] = e.to_center;
   }
+  if (kind == kCycle) dirty[nd++] = anchor;  // the inserted row was never repaired
   // allotment bookkeeping (apply_path_edges, refine.hpp:134-164): warp 0
   // of rank 0, one lane per path edge, so the global accesses of all edges
   // overlap (a simple path moves distinct demands between distinct centers;
@@ -1278,7 +1281,15 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       else lc[kLcPaths] += 1;
     }
   }
-  if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+  // the π-repair search's sources (the dirty rows) travel in this exchange:
+  // the labels of the finished search are no longer read (reconstruct's
+  // exchange is behind us), and without rescans the repair starts right
+  // after it
+  X.delta = X.delta_main;
+  reset_labels(X, 0);
+  __syncthreads();
+  publish_sources(X, dirty, nd, kRepair);
+  __syncthreads();
   PROF_MARK(X, 0);   // T1
   // (no list validation here: until this barrier the lead's home[] writes
   // and, after it, other CTAs' T3 rescans race with a reader of the lists)
@@ -1519,14 +1530,19 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       if (j < jlo || j >= jhi) continue;
       const int64_t idx = static_cast<int64_t>(e.from_center) * k + j;
       const int64_t m = A.M[idx];
-      const int64_t* mx = A.MX + idx * 3;
-      const int len = (m != kEmpty) + (mx[0] != kEmpty) + (mx[1] != kEmpty) + (mx[2] != kEmpty);
+      const int len = (m != kEmpty) + (*mx_slot(A, idx, 0) != kEmpty) + (*mx_slot(A, idx, 1) != kEmpty) +
+                      (*mx_slot(A, idx, 2) != kEmpty);
       A.LN[idx] = static_cast<uint8_t>(len | (len < kTopK ? 8 : 0));
       if (X.tile) X.wt[static_cast<int64_t>(e.from_center) * X.wst + (j - X.v0)] = key16(m);
     }
   }
   __syncthreads();
   validate_lists(X, 2);
+  if (total > 0) {  // the T3 exchange came after the sources: publish them again
+    publish_sources(X, dirty, nd, kRepair);
+    __syncthreads();
+    exchange(X);
+  }
   if (X.lead) S.lc[kLcTindex] += gtimer() - t0;
   return nd;
 }
@@ -1957,18 +1973,12 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       if (X.lead) check_path_sum(X, kind, s, len, refund, sl);
       // a mismatch is raised at the next exchange; every CTA still runs
       // apply so the cluster barriers stay matched
-      int nd = apply(X, kind, len, lab_d(sl), dirty);
+      // apply ends with the π-repair search's sources (the dirty rows) exchanged
+      apply(X, kind, len, lab_d(sl), dirty, s);
       PROF_MARK(X, 11);
-      if (kind == kCycle) dirty[nd++] = s;  // the inserted row was never repaired
       // ---- π repair from the dirty rows: a search of kind kRepair ----
       after = kind == kCycle ? kStAfterCycle : kStPathEnd;
       applied = true;
-      X.delta = X.delta_main;
-      reset_labels(X, 0);
-      __syncthreads();
-      publish_sources(X, dirty, nd, kRepair);
-      __syncthreads();
-      exchange(X);
       kind = kRepair;
       refund = 0;
       bound = 0;

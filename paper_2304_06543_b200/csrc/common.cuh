@@ -187,7 +187,7 @@ struct EngineArgs {
   int32_t add_cap;        // per-center capacity of the add lists
   int32_t* add_ids;       // [k][add_cap]: demands that moved to center u this launch
   int32_t* add_cnt;       // [k]: appends per center (past add_cap: use the move log)
-  int64_t* MX;            // k*k*3: 2nd..4th smallest transfer per entry
+  int64_t* MX;            // 3 planes of k*k: 2nd..4th smallest transfer per entry
   uint8_t* LN;            // k*k: list length | complete << 3
   int32_t debug_checks;   // validate engine invariants after each phase
   int32_t pad4;

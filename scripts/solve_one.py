@@ -24,6 +24,8 @@ p.add_argument("--seed", type=int, default=20250)
 p.add_argument("--theta", default="8/10")
 p.add_argument("--reps", type=int, default=1)
 p.add_argument("--golden", default=None)
+p.add_argument("--prefix", type=int, default=0,
+               help="solve only the first N arrivals (lbdd_b200_solve_prefix): large-k samples")
 p.add_argument("--scan", action="store_true", help="also time the build_index scan")
 p.add_argument("--road", action="store_true",
                help="configs[3]-style road-network instance (RoadSpec, host-generated)")
@@ -47,7 +49,8 @@ else:
 for r in range(a.reps):
     t = time.time()
     try:
-        rep = S.asral_solve(dev, want_assignment=bool(a.golden))
+        rep = (S.asral_prefix(dev, a.prefix) if a.prefix
+               else S.asral_solve(dev, want_assignment=bool(a.golden)))
     except Exception as e:
         print(f"rep {r} FAILED after {time.time() - t:.1f}s: {e!r}", flush=True)
         continue

@@ -361,23 +361,26 @@ __device__ __forceinline__ void list_store(const EngineArgs& A, int64_t idx, con
   *mx_slot(A, idx, 2) = t.e[3];
   A.LN[idx] = static_cast<uint8_t>(t.len | (t.complete ? 8 : 0));
 }
-// returns true when the head changed
+// returns true when the head changed. Fixed indices only (compare-and-swap
+// insertion; slots past `len` hold kEmpty), so a TopK stays in registers
+// instead of a dynamically indexed local-memory array.
 __device__ __forceinline__ bool list_insert(TopK& t, int64_t v) {
   if (!t.complete && t.len == 0) return false;  // unknown minimum: a rescan follows
-  if (!t.complete && v > t.e[t.len - 1]) return false;
-  if (t.complete && t.len == kTopK && v > t.e[kTopK - 1]) {
+  const int64_t last = t.len <= 1 ? t.e[0] : t.len == 2 ? t.e[1] : t.len == 3 ? t.e[2] : t.e[3];
+  if (!t.complete && v > last) return false;
+  if (t.complete && t.len == kTopK) {
     t.complete = false;  // one more member than the list holds
-    return false;
+    if (v > t.e[kTopK - 1]) return false;
   }
-  if (t.complete && t.len == kTopK) t.complete = false;
-  int p = t.len < kTopK ? t.len : kTopK - 1;  // slot freed for the insert
-  while (p > 0 && t.e[p - 1] > v) {
-    t.e[p] = t.e[p - 1];
-    --p;
+  const bool head = v < t.e[0];
+#pragma unroll
+  for (int i = 0; i < kTopK; ++i) {
+    const int64_t lo = min(t.e[i], v);
+    v = max(t.e[i], v);
+    t.e[i] = lo;
   }
-  t.e[p] = v;
   if (t.len < kTopK) ++t.len;
-  return p == 0;
+  return head;
 }
 // Concurrent rescan insert into an emptied list (all of M, MX start at
 // kEmpty): atomicMin at slot 0, the larger value carries on to the next
@@ -400,11 +403,15 @@ __device__ __forceinline__ void list_sink(const EngineArgs& A, int64_t idx, int6
 // changed) | (2 when a rescan is needed)
 __device__ __forceinline__ int list_remove(TopK& t, int32_t demand) {
   int p = -1;
-  for (int i = 0; i < t.len; ++i) {
-    if (t.e[i] != kEmpty && transfer_demand(t.e[i]) == demand) p = i;
+#pragma unroll
+  for (int i = 0; i < kTopK; ++i) {
+    if (i < t.len && t.e[i] != kEmpty && transfer_demand(t.e[i]) == demand) p = i;
   }
   if (p < 0) return 0;
-  for (int i = p; i + 1 < kTopK; ++i) t.e[i] = t.e[i + 1];
+#pragma unroll
+  for (int i = 0; i + 1 < kTopK; ++i) {
+    if (i >= p) t.e[i] = t.e[i + 1];
+  }
   t.e[kTopK - 1] = kEmpty;
   --t.len;
   int r = p == 0 ? 5 : 4;

@@ -1627,6 +1627,13 @@ __device__ __forceinline__ void prefetch_row(Ctx& X, int64_t a) {
   if (threadIdx.x == blockDim.x - 1) cp_async4(&dst[X.s], &row[s]);
 }
 
+// the stage after a search: through kStCertify when invariants are checked
+__device__ __forceinline__ int certify_then(const Ctx& X, int& cert_next, int next) {
+  if (!X.A.check_invariants) return next;
+  cert_next = next;
+  return 5;  // kStCertify
+}
+
 }  // namespace cl
 
 // Shared memory: see cl::carve.
@@ -1788,12 +1795,13 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
   //   kStAfterCycle  overload check (asral)
   //   kStPathBound   path bound C; start the path search or give up
   //   kStPathEnd     fixpoint loop (refine_to_fixpoint)
-  enum Stage : int { kStArrival, kStSearch, kStAfterCycle, kStPathBound, kStPathEnd };
+  enum Stage : int { kStArrival, kStSearch, kStAfterCycle, kStPathBound, kStPathEnd, kStCertify };
+  static_assert(kStCertify == 5, "certify_then returns the stage id of kStCertify");
   int stage = kStArrival;
   int64_t a = A.a_begin;
   int32_t d = 0, s = 0;
   int64_t cost = 0, cap = 0, refund = 0, bound = 0, sink_inc = kLabInf;
-  int kind = kCycle, after = kStAfterCycle;
+  int kind = kCycle, after = kStAfterCycle, cert_next = kStArrival;
   bool applied = false;
   int64_t t_search = 0;
   while (!X.err) {
@@ -1929,8 +1937,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
         apply_repair(X);  // π += min(0, d) over the explored region
         __syncthreads();
         PROF_MARK(X, 6);  // repairs
-        certify(X);
-        stage = after;
+        stage = certify_then(X, cert_next, after);
         continue;
       }
       if (X.lead) X.S.lc[kLcTbf] += gtimer() - t_search;
@@ -1945,13 +1952,11 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
           if (rounds > 0) apply_repair(X);
           __syncthreads();
           PROF_MARK(X, 6);
-          certify(X);
-          stage = kStAfterCycle;
+          stage = certify_then(X, cert_next, kStAfterCycle);
         } else {
           PROF_MARK(X, 8);  // path search
-          certify(X);
           applied = false;
-          stage = kStPathEnd;
+          stage = certify_then(X, cert_next, kStPathEnd);
         }
         continue;
       }
@@ -2055,9 +2060,8 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       for (int r = 0; r < X.csz; ++r) cmin = min(cmin, S.all[r].val);
       if (!(cmin != kEmpty && cmin - pis_now < 0) || X.err) {
         if (X.lead) X.dbg[9] += 1;  // pruned
-        certify(X);
         applied = false;
-        stage = kStPathEnd;
+        stage = certify_then(X, cert_next, kStPathEnd);
         continue;
       }
       const int64_t C = cmin - pis_now;
@@ -2073,6 +2077,12 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       sink_inc = kHop - bound;  // path graph: rc_pen >= C into anchor-in
       t_search = gtimer();
       stage = kStSearch;
+      continue;
+    }
+
+    if (stage == kStCertify) {  // check_invariants only: the one copy of certify
+      certify(X);
+      stage = cert_next;
       continue;
     }
 

@@ -17,9 +17,10 @@
 //    each node v with parent = the smallest u such that
 //    d*(u) + w(u,v) = d*(v) and h*(u) = h*(v) - 1, where h* is the fewest
 //    edges among shortest paths (the round in which d*(v) is first reached).
-//    Lexicographic labels (d, h) computed by ANY label-correcting order are
-//    unique, so a frontier search with packed (d << 16 | h) labels and the
-//    parent rule applied afterwards returns the reference's path bit for bit.
+//    Lexicographic labels (d, h, parent) computed by ANY label-correcting
+//    order are unique, so a frontier search with packed
+//    (d << 26 | h << 13 | parent) labels returns the reference's path bit
+//    for bit.
 //  * π is repaired after every change of Γ: D(v) = min(0, min_{x in X}
 //    dist_rc(x, v)) over the rows X that may now violate it (the anchor after
 //    an insert, the receiving centers of an applied path) is again a bounded
@@ -30,9 +31,12 @@
 //
 // Node ownership: node v (0..k, k = anchor-in) belongs to CTA v / s, s =
 // ceil((k+1)/CS); the owner holds its label, its π and its "changed" flag,
-// and relaxes every edge INTO its nodes, so label updates are CTA-local
-// shared-memory atomics. Sources of the next round are published as
-// (node, label, π, placeholder flag) lists read through DSMEM.
+// and relaxes every edge INTO its nodes (row partials folded by the owner,
+// no shared-memory atomics on labels); edges INTO anchor-in are evaluated
+// by the owners of their sources. Sources of the next round travel as
+// (node, label + π, placeholder flag) entries pushed into every CTA's inbox
+// (st.async + round mbarriers during searches, DSMEM stores + cluster
+// barrier around the phases that order global memory).
 #include <cooperative_groups.h>
 
 #include "common.cuh"

@@ -52,6 +52,12 @@ constexpr int kStage = 256;            // frontier entries staged per pass
 constexpr int16_t kNoKey16 = INT16_MAX;  // "no demand at the source" in the tile
 constexpr int kMaxSeg = 32;            // source rows rescanned per apply via the index
 constexpr int kRowSlots = 8;           // source rows of a row-mode rescan (column bitmaps)
+// Row-mode rescans (member rows streamed over the owner's columns in 16 B
+// pieces) measured slower than gathering the invalidated columns at every
+// threshold once the add lists made candidate sets small (200K x 1000:
+// 10.88 s with row mode at >= 4 columns per 16 pieces, 10.52 s without;
+// k = 2000 6.60 -> 6.39 s; k = 5000 unchanged); kept compiled out.
+constexpr bool kRowMode = false;
 constexpr int kMaxMine = 1024;
 // frontier entries one CTA pushes per exchange (inbox slots per source):
 // changed nodes past it stay pending for a later round -- the Δ-stepping
@@ -1377,7 +1383,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     bool rowmode = false;
     if (!generic) {
       for (int g = 0; g < nseg; ++g) maxmine = max(maxmine, S.segmine[g]);
-      rowmode = nseg <= kRowSlots && 4 * maxmine >= npc;
+      rowmode = kRowMode && nseg <= kRowSlots && 4 * maxmine >= npc;
       if (rowmode) {
         for (int w = threadIdx.x; w < nseg * nw32; w += blockDim.x) S.bits[w] = 0;
         __syncthreads();

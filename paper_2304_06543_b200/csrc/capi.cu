@@ -697,9 +697,9 @@ void reset_engine_state(lbdd_b200_instance* I, int64_t delta0) {
   CUDA_OK(cudaMemsetAsync(I->rowver.p, 0, sizeof(int32_t) * (k + 1), I->stream));
   CUDA_OK(cudaMemsetAsync(I->pi.p, 0, sizeof(int64_t) * (k + 1), I->stream));
   // top-4 lists of the cluster engine: empty and complete
-  I->MX.ensure(static_cast<size_t>(k) * k * 3);
+  I->MX.ensure(static_cast<size_t>(k) * k * (cl::kTopK - 1));
   I->LN.ensure(static_cast<size_t>(k) * k);
-  fill64(I, I->MX.p, k * k * 3, kEmpty);
+  fill64(I, I->MX.p, k * k * (cl::kTopK - 1), kEmpty);
   CUDA_OK(cudaMemsetAsync(I->LN.p, 8, static_cast<size_t>(k) * k, I->stream));
   EngineCtl ctl;
   std::memset(&ctl, 0, sizeof(ctl));

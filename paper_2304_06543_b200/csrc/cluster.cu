@@ -344,7 +344,11 @@ __device__ __forceinline__ int64_t refund_penalty(Ctx& X, int s, int64_t load) {
 // Invariant: the list is exactly the `length` smallest transfers of the
 // heap (subspace.hpp:26-231), so removing the head promotes the true next
 // minimum; a rescan is needed only when an incomplete list runs empty.
-constexpr int kTopK = 4;
+#ifndef LBDD_TOPK
+#define LBDD_TOPK 4
+#endif
+constexpr int kTopK = LBDD_TOPK;  // list depth (M head + kTopK - 1 MX planes); LN holds len in 3 bits
+static_assert(kTopK >= 2 && kTopK <= 7, "list length must fit LN's 3 bits");
 struct TopK {
   int64_t e[kTopK];
   int len;
@@ -356,9 +360,8 @@ __device__ __forceinline__ int64_t* mx_slot(const EngineArgs& A, int64_t idx, in
 __device__ __forceinline__ TopK list_load(const EngineArgs& A, int64_t idx) {
   TopK t;
   t.e[0] = A.M[idx];
-  t.e[1] = *mx_slot(A, idx, 0);
-  t.e[2] = *mx_slot(A, idx, 1);
-  t.e[3] = *mx_slot(A, idx, 2);
+#pragma unroll
+  for (int i = 1; i < kTopK; ++i) t.e[i] = *mx_slot(A, idx, i - 1);
   const uint8_t ln = A.LN[idx];
   t.len = ln & 7;
   t.complete = (ln & 8) != 0;
@@ -366,9 +369,8 @@ __device__ __forceinline__ TopK list_load(const EngineArgs& A, int64_t idx) {
 }
 __device__ __forceinline__ void list_store(const EngineArgs& A, int64_t idx, const TopK& t) {
   A.M[idx] = t.e[0];
-  *mx_slot(A, idx, 0) = t.e[1];
-  *mx_slot(A, idx, 1) = t.e[2];
-  *mx_slot(A, idx, 2) = t.e[3];
+#pragma unroll
+  for (int i = 1; i < kTopK; ++i) *mx_slot(A, idx, i - 1) = t.e[i];
   A.LN[idx] = static_cast<uint8_t>(t.len | (t.complete ? 8 : 0));
 }
 // returns true when the head changed. Fixed indices only (compare-and-swap
@@ -376,7 +378,10 @@ __device__ __forceinline__ void list_store(const EngineArgs& A, int64_t idx, con
 // instead of a dynamically indexed local-memory array.
 __device__ __forceinline__ bool list_insert(TopK& t, int64_t v) {
   if (!t.complete && t.len == 0) return false;  // unknown minimum: a rescan follows
-  const int64_t last = t.len <= 1 ? t.e[0] : t.len == 2 ? t.e[1] : t.len == 3 ? t.e[2] : t.e[3];
+  int64_t last = t.e[0];
+#pragma unroll
+  for (int i = 1; i < kTopK; ++i)
+    if (i < t.len) last = t.e[i];
   if (!t.complete && v > last) return false;
   if (t.complete && t.len == kTopK) {
     t.complete = false;  // one more member than the list holds
@@ -399,7 +404,7 @@ __device__ __forceinline__ bool list_insert(TopK& t, int64_t v) {
 // the four smallest; the prefilter reads slot 3 at L2 (a stale larger value
 // only costs the cascade).
 __device__ __forceinline__ void list_sink(const EngineArgs& A, int64_t idx, int64_t x) {
-  if (x >= static_cast<int64_t>(__ldcg(reinterpret_cast<const long long*>(mx_slot(A, idx, 2))))) return;
+  if (x >= static_cast<int64_t>(__ldcg(reinterpret_cast<const long long*>(mx_slot(A, idx, kTopK - 2))))) return;
   int64_t old = atomicMin(reinterpret_cast<long long*>(&A.M[idx]), static_cast<long long>(x));
   if (old == x) return;
   x = max(old, x);
@@ -1547,8 +1552,9 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       if (j < jlo || j >= jhi) continue;
       const int64_t idx = static_cast<int64_t>(e.from_center) * k + j;
       const int64_t m = A.M[idx];
-      const int len = (m != kEmpty) + (*mx_slot(A, idx, 0) != kEmpty) + (*mx_slot(A, idx, 1) != kEmpty) +
-                      (*mx_slot(A, idx, 2) != kEmpty);
+      int len = m != kEmpty;
+#pragma unroll
+      for (int q = 0; q < kTopK - 1; ++q) len += *mx_slot(A, idx, q) != kEmpty;
       A.LN[idx] = static_cast<uint8_t>(len | (len < kTopK ? 8 : 0));
       if (X.tile) X.wt[static_cast<int64_t>(e.from_center) * X.wst + (j - X.v0)] = key16(m);
     }

@@ -770,7 +770,7 @@ size_t cluster_smem_bytes(int k, int s, int block, bool tile) {
          4 * static_cast<size_t>(cl::kRowSlots) * ((k + 31) / 32) +
          (tile ? 2 * static_cast<size_t>(k) * s : 0) + static_cast<size_t>(s) + 16 +
          8 * static_cast<size_t>(s) + 8 * static_cast<size_t>(std::max(block, s)) + 8 * 4 * 32 +
-         4 * 4 * cl::kMaxCS;
+         4 * 4 * cl::kMaxCS + sizeof(PathEdge) * cl::kPathCache;
 }
 
 bool cluster_engine_fits(int k) {

@@ -59,6 +59,7 @@ constexpr int kRowSlots = 8;           // source rows of a row-mode rescan (colu
 // k = 2000 6.60 -> 6.39 s; k = 5000 unchanged); kept compiled out.
 constexpr bool kRowMode = false;
 constexpr int kMaxMine = 1024;
+constexpr int kPathCache = 64;         // path edges mirrored in shared memory (the rest: global only)
 // frontier entries one CTA pushes per exchange (inbox slots per source):
 // changed nodes past it stay pending for a later round -- the Δ-stepping
 // hold-back mechanism -- so shared memory no longer grows with k
@@ -111,7 +112,8 @@ struct CS {           // shared-memory layout of one CTA
   int64_t* pis;       // [s]
   Pair2<FEntry> inbox;  // [kMaxCS * cin] each: entries pushed by CTA r at r * cin
   Pair2<Pub> pub;      // [1] each
-  PathEdge* path;     // [k + 1]
+  PathEdge* path;     // [k + 1] (global, one slice per CTA)
+  PathEdge* pc;       // [kPathCache] shared-memory copy of the first path edges (path_at)
   uint8_t* chg;       // [s]
   int32_t* qd;        // [blockDim] rescan queue
   int32_t* qs;        // [blockDim]
@@ -147,6 +149,14 @@ struct CS {           // shared-memory layout of one CTA
                       // (tile mode: all keys fit in int16)
 };
 
+// The applied path: global slice S.path (any length), its first kPathCache
+// edges mirrored in shared memory so that apply / T1 / T3 read them without
+// an L2 round trip.
+__device__ __forceinline__ PathEdge path_at(const CS& S, int i) { return i < kPathCache ? S.pc[i] : S.path[i]; }
+__device__ __forceinline__ void path_set(const CS& S, int i, const PathEdge& e) {
+  S.path[i] = e;
+  if (i < kPathCache) S.pc[i] = e;
+}
 // host mirror: cluster_smem_bytes() in capi.cu
 __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   CS S;
@@ -163,6 +173,7 @@ __device__ __forceinline__ CS carve(unsigned char* p, int k, int s, bool tile) {
   S.part = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(max(static_cast<int>(blockDim.x), s));
   S.wred = reinterpret_cast<int64_t*>(p); p += 8 * 4 * 32;
   S.rin = reinterpret_cast<uint32_t*>(p); p += 4 * 2 * kMaxCS;
+  S.pc = reinterpret_cast<PathEdge*>(p); p += sizeof(PathEdge) * kPathCache;
   S.rbar = reinterpret_cast<uint32_t*>(p); p += 4 * 2 * kMaxCS;
   S.seg = reinterpret_cast<int32_t*>(p); p += 4 * 3 * kMaxSeg;
   S.mine = reinterpret_cast<int32_t*>(p); p += 4 * kMaxMine;
@@ -476,7 +487,7 @@ __device__ void validate_lists(Ctx& X, int where) {
                e == kEmpty ? -1 : transfer_demand(e), e == kEmpty ? -2 : A.home[transfer_demand(e)]);
       }
       for (int i = 0; i < k + 1 && i < 12; ++i) {
-        const PathEdge pe = X.S.path[i];
+        const PathEdge pe = path_at(X.S, i);
         printf("  path[%d] %d -> %d kind %d demand %d inv_cnt %d\n", i, pe.from_center, pe.to_center,
                pe.kind, pe.demand, A.inv_cnt[i]);
       }
@@ -1132,7 +1143,7 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
       e.to_center = v == X.k ? anchor : v;
       e.demand = -1;
       e.kind = kEdgeNone;
-      S.path[len++] = e;  // reversed order for now
+      path_set(S, len++, e);  // reversed order for now
       if (u != anchor) {
         const int r = u / X.s;
         lv = X.cluster.map_shared_rank(S.lab, r)[u - r * X.s];
@@ -1150,7 +1161,7 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
   }
   // edge kinds and transfer words (the first recorded edge enters anchor-in)
   for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    PathEdge e = S.path[i];
+    PathEdge e = path_at(S, i);
     if (kind == kPath && i == 0) {
       e.kind = kEdgePenalty;
     } else {
@@ -1159,14 +1170,14 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
       e.kind = pair_kind(m, dum);
       if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
     }
-    S.path[i] = e;
+    path_set(S, i, e);
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // reverse into path order
     for (int i = 0; i < len / 2; ++i) {
-      const PathEdge t = S.path[i];
-      S.path[i] = S.path[len - 1 - i];
-      S.path[len - 1 - i] = t;
+      const PathEdge t = path_at(S, i);
+      path_set(S, i, path_at(S, len - 1 - i));
+      path_set(S, len - 1 - i, t);
     }
     S.pub[X.par]->count = 0;
   }
@@ -1192,19 +1203,19 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   // removal before the gain (as the reference's per-edge order leaves it).
   const int jlo = X.v0, jhi = min(X.v1, k);
   const int ncol = max(0, jhi - jlo);
-  const PathEdge last = S.path[len - 1];
-  const bool extra = last.kind == kEdgeTransfer && last.to_center != S.path[0].from_center;
+  const PathEdge last = path_at(S, len - 1);
+  const bool extra = last.kind == kEdgeTransfer && last.to_center != path_at(S, 0).from_center;
   const int ntask = len + (extra ? 1 : 0);
   for (int q = threadIdx.x; q < ntask * ncol; q += blockDim.x) {
     const int p = q / ncol;
     const int j = jlo + (q - p * ncol);
     int row, rm = -1, in = -1;  // row; removal edge; gain edge
     if (p < len) {
-      const PathEdge e = S.path[p];
+      const PathEdge e = path_at(S, p);
       row = e.from_center;
       if (e.kind == kEdgeTransfer) rm = p;
       const int pi = p > 0 ? p - 1 : len - 1;
-      const PathEdge f = S.path[pi];
+      const PathEdge f = path_at(S, pi);
       if (f.kind == kEdgeTransfer && f.to_center == row && (p > 0 || len > 1 || pi != p)) in = pi;
     } else {
       row = last.to_center;
@@ -1214,14 +1225,14 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     const int64_t idx = static_cast<int64_t>(row) * k + j;
     int32_t din = -1, vin = 0;
     if (in >= 0) {
-      din = S.path[in].demand;
+      din = path_at(S, in).demand;
       const int32_t* rowin = row_of(A.rows, din);
       vin = rowin[j] - rowin[row];
     }
     TopK t = list_load(A, idx);
     bool changed = false, head = false;
     if (rm >= 0) {
-      const int r = list_remove(t, S.path[rm].demand);
+      const int r = list_remove(t, path_at(S, rm).demand);
       if (r != 0) {
         changed = true;
         head = (r & 1) != 0;
@@ -1240,7 +1251,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   }
   int nd = 0;
   for (int i = 0; i < len; ++i) {
-    const PathEdge e = S.path[i];
+    const PathEdge e = path_at(S, i);
     if (e.kind == kEdgeTransfer || e.kind == kEdgeDummy) dirty[nd++] = e.to_center;
   }
   if (kind == kCycle) dirty[nd++] = anchor;  // the inserted row was never repaired
@@ -1260,7 +1271,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
       const int i = i0 + lane;
       PathEdge e;
       e.kind = kEdgeNone;
-      if (i < len) e = S.path[i];
+      if (i < len) e = path_at(S, i);
       const bool tr = e.kind == kEdgeTransfer;
       const unsigned bt = __ballot_sync(0xffffffffu, tr);
       if (tr) {
@@ -1281,7 +1292,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     if (lane == 0) {
       // placeholder moves (strict): in path order, a center's gain before its loss
       for (int i = 0; i < len; ++i) {
-        const PathEdge e = S.path[i];
+        const PathEdge e = path_at(S, i);
         if (e.kind != kEdgeDummy) continue;
         if (A.dummies == nullptr || A.dummies[e.from_center] <= 0) {
           set_err(X, kErrPlaceholder, e.from_center);
@@ -1326,7 +1337,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   // entries of ITS columns (the owner is the only writer of its lists in
   // this phase), so the member-row reads spread over the whole cluster.
   int total = 0;
-  for (int i = 0; i < len; ++i) total += (S.path[i].kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
+  for (int i = 0; i < len; ++i) total += (path_at(S, i).kind == kEdgeTransfer) ? A.inv_cnt[i] : 0;
   if (total > 0) {
     int32_t* seg = S.seg;  // [3 * kMaxSeg]: (slot, prefix end, bucket count)
     int nseg = 0;
@@ -1336,9 +1347,9 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     bool allscan = A.bk_ids == nullptr || *A.log_n > A.log_cap;
     bool uselog = false;
     for (int i = 0; i < len && !allscan; ++i) {
-      if (S.path[i].kind != kEdgeTransfer || A.inv_cnt[i] == 0) continue;
+      if (path_at(S, i).kind != kEdgeTransfer || A.inv_cnt[i] == 0) continue;
       if (nseg == kMaxSeg) { allscan = true; break; }
-      const int u = S.path[i].from_center;
+      const int u = path_at(S, i).from_center;
       const int32_t nb = A.bk_off[u + 1] - A.bk_off[u];
       const int32_t na = A.add_cnt != nullptr ? A.add_cnt[u] : 0;
       if (na > A.add_cap) uselog = true;
@@ -1429,7 +1440,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
     int maxcnt = 0;
     if (full) {
       for (int i = 0; i < len; ++i) {
-        if (S.path[i].kind == kEdgeTransfer) maxcnt = max(maxcnt, A.inv_cnt[i]);
+        if (path_at(S, i).kind == kEdgeTransfer) maxcnt = max(maxcnt, A.inv_cnt[i]);
       }
     }
     for (int64_t base = cbase; base < ncand; base += stride) {
@@ -1449,7 +1460,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           int g = 0;
           while (x >= seg[3 * g + 1]) ++g;
           const int slot = seg[3 * g];
-          const int u = S.path[slot].from_center;
+          const int u = path_at(S, slot).from_center;
           const int64_t off = x - (g == 0 ? 0 : seg[3 * g - 2]);
           const int32_t nb = seg[3 * g + 2];
           dd = off < nb ? A.bk_ids[A.bk_off[u] + off]
@@ -1474,7 +1485,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           S.qd[q] = dd;
           S.qs[q] = sl;  // full: path slot; else: segment
           S.qh[q] = row_of(A.rows, dd)[
-                         S.path[full ? sl : seg[3 * sl]].from_center];
+                         path_at(S, full ? sl : seg[3 * sl]).from_center];
         }
       }
       __syncthreads();
@@ -1491,7 +1502,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           const int cnt = A.inv_cnt[sl2];
           if (xx >= cnt) continue;
           const int32_t d2 = S.qd[q];
-          const int u = S.path[sl2].from_center;
+          const int u = path_at(S, sl2).from_center;
           const int j = A.inv_cols[static_cast<int64_t>(sl2) * k + xx];
           const int32_t* row = row_of(A.rows, d2);
           list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
@@ -1507,7 +1518,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           if ((word & 15u) == 0) continue;
           const int32_t d2 = S.qd[q];
           const int32_t hv = S.qh[q];
-          const int u = S.path[seg[3 * g]].from_center;
+          const int u = path_at(S, seg[3 * g]).from_center;
           const int4 x4 = reinterpret_cast<const int4*>(row_of(A.rows, d2))[c4];
           const int32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
@@ -1527,7 +1538,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
           if (xx >= o1 - o0) continue;
           const int j = S.mine[o0 + xx];
           const int32_t d2 = S.qd[q];
-          const int u = S.path[seg[3 * g]].from_center;
+          const int u = path_at(S, seg[3 * g]).from_center;
           const int32_t* row = row_of(A.rows, d2);
           list_sink(A, static_cast<int64_t>(u) * k + j, pack_transfer(row[j] - S.qh[q], d2));
         }
@@ -1544,7 +1555,7 @@ __device__ __forceinline__ int apply(Ctx& X, int kind, int len, int64_t cost, in
   // rescanned entries now hold the (up to) four smallest transfers of their
   // row: complete when fewer than four exist; refresh my tile columns
   for (int i = 0; i < len; ++i) {
-    const PathEdge e = S.path[i];
+    const PathEdge e = path_at(S, i);
     if (e.kind != kEdgeTransfer) continue;
     const int cnt = A.inv_cnt[i];
     for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
@@ -1601,7 +1612,7 @@ __device__ __forceinline__ void check_path_sum(Ctx& X, int kind, int anchor, int
   const EngineArgs& A = X.A;
   int64_t sum = 0;
   for (int i = 0; i < len; ++i) {
-    const PathEdge e = X.S.path[i];
+    const PathEdge e = path_at(X.S, i);
     if (e.kind == kEdgeTransfer) {
       const int32_t* row = row_of(A.rows, e.demand);
       sum += static_cast<int64_t>(row[e.to_center]) - row[e.from_center];
@@ -1990,7 +2001,7 @@ __global__ void __launch_bounds__(LBDD_CLUSTER_THREADS, 1) cluster_engine_kernel
       const int len = reconstruct(X, kind, s, refund, sl);
       PROF_MARK(X, 10);
       if (len == 0 || X.err) break;
-      if (kind == kPath && X.S.path[len - 1].kind != kEdgePenalty) {
+      if (kind == kPath && path_at(X.S, len - 1).kind != kEdgePenalty) {
         if (X.lead) set_err(X, kErrPenaltyEdge, len);
         X.err = 1;
         break;

@@ -1159,27 +1159,49 @@ __device__ __forceinline__ int reconstruct(Ctx& X, int kind, int anchor, int64_t
     X.err = 1;
     return 0;
   }
-  // edge kinds and transfer words (the first recorded edge enters anchor-in)
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    PathEdge e = path_at(S, i);
-    if (kind == kPath && i == 0) {
-      e.kind = kEdgePenalty;
-    } else {
-      const int64_t m = A.M[static_cast<int64_t>(e.from_center) * A.k + e.to_center];
-      const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[e.from_center] > 0;
-      e.kind = pair_kind(m, dum);
-      if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
+  // edge kinds and transfer words (the first recorded edge enters anchor-in),
+  // each edge written straight to its place in path order (read all, CTA
+  // barrier, write all: the reversal is in place)
+  const int per = (len + blockDim.x - 1) / blockDim.x;  // edges per thread (1 unless len > blockDim)
+  if (per == 1) {
+    PathEdge e;
+    const int i = threadIdx.x;
+    if (i < len) {
+      e = path_at(S, i);
+      if (kind == kPath && i == 0) {
+        e.kind = kEdgePenalty;
+      } else {
+        const int64_t m = A.M[static_cast<int64_t>(e.from_center) * A.k + e.to_center];
+        const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[e.from_center] > 0;
+        e.kind = pair_kind(m, dum);
+        if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
+      }
     }
-    path_set(S, i, e);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // reverse into path order
-    for (int i = 0; i < len / 2; ++i) {
-      const PathEdge t = path_at(S, i);
-      path_set(S, i, path_at(S, len - 1 - i));
-      path_set(S, len - 1 - i, t);
+    __syncthreads();
+    if (i < len) path_set(S, len - 1 - i, e);
+    if (threadIdx.x == 0) S.pub[X.par]->count = 0;
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      PathEdge e = path_at(S, i);
+      if (kind == kPath && i == 0) {
+        e.kind = kEdgePenalty;
+      } else {
+        const int64_t m = A.M[static_cast<int64_t>(e.from_center) * A.k + e.to_center];
+        const bool dum = kind == kCycle && A.dummies != nullptr && A.dummies[e.from_center] > 0;
+        e.kind = pair_kind(m, dum);
+        if (e.kind == kEdgeTransfer) e.demand = transfer_demand(m);
+      }
+      path_set(S, i, e);
     }
-    S.pub[X.par]->count = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // reverse into path order
+      for (int i = 0; i < len / 2; ++i) {
+        const PathEdge t = path_at(S, i);
+        path_set(S, i, path_at(S, len - 1 - i));
+        path_set(S, len - 1 - i, t);
+      }
+      S.pub[X.par]->count = 0;
+    }
   }
   exchange(X);
   return X.err ? 0 : len;
